@@ -1,0 +1,184 @@
+/*
+ * bnfft -- B200-native hot path of Algorithm 2, "NFFT-like procedure for bandlimited
+ * functions" (Kircheis & Potts, arXiv 2502.07155).  C ABI: plain pointers and sizes.
+ *
+ * Problem (Algorithm 2): given samples f^(k),
+ * k in I_M = Z^d cap [-M/2, M/2)^d of the Fourier transform of a bandlimited f, and
+ * nodes x_j in R^d, compute
+ *     step 0(a)  psi^(k), k in I_M
+ *     step 1     theta^(k) = f^(k)/psi^(k) on I_M, 0 on I_L \ I_M
+ *     step 2     theta_l = L^{-d} sum_{k in I_L} theta^(k) e^{2 pi i k.l/L}, l in I_L
+ *     step 3     f_j = sum_{l in J_{L,m}(x_j) cap I_L} theta_l psi(x_j - l/L)
+ * with the regularized sinc psi(x) = sinc(L pi x) phi(x) (eq. sinc_reg) and a
+ * window phi in Phi_{m,L}: sinh-type (eq. varphisinh), continuous
+ * Kaiser-Bessel or the Gaussian of reading A2.  Matrix form:
+ * f = Psi F D_psihat f^ (eq. function_eval).
+ *
+ * Readings where the paper is silent: L = M_sigma = 2 ceil(ceil(sigma M)/2)
+ * (A7); default shape beta = pi m (1 - M/L) (A1), Gaussian s = sqrt(m/(pi L (L-M))) (A2);
+ * tensor-product windows (A3); psi^ by 64-point Gauss-Legendre after t = (m/L) sin(theta) (A4);
+ * nodes accepted on [-1/2, 1/2)^d with the literal I_L-truncated sum (A5).
+ *
+ * Execution model: every step runs on the GPU given at plan creation.  Step 2 calls cuFFT
+ * (a separately timed stage, BASELINE north_star (c)); all other steps are this library's
+ * own sm_100a kernels.  There is no CPU fallback: without a CUDA device every call that
+ * would compute returns BNFFT_E_CUDA.
+ *
+ * Ownership: the caller owns every pointer it passes; the plan owns its device buffers
+ * (psi^ table, FFT input/output grids, sorted nodes, permutation, bin offsets, scratch).
+ * Thread safety: a plan is not re-entrant; distinct plans are independent.
+ * Errors: every entry point returns 0 (BNFFT_OK) or a negative bnfft_status; no entry point
+ * aborts the process.  bnfft_last_error() gives a human-readable detail for the calling thread.
+ */
+#ifndef BNFFT_H
+#define BNFFT_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BNFFT_API __attribute__((visibility("default")))
+#else
+#define BNFFT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BNFFT_OK = 0,
+  BNFFT_E_BAD_DIM = -1,                  /* d not in 1..3                                   */
+  BNFFT_E_BAD_BANDWIDTH = -2,            /* M odd or < 2 ("M in 2N")                   */
+  BNFFT_E_BAD_SIGMA = -3,                /* sigma < 1 or not finite                   */
+  BNFFT_E_TRUNCATION_TOO_LARGE = -4,     /* m < 1 or 2m >= L ("2m << L")               */
+  BNFFT_E_BAD_WINDOW_PARAM = -5,         /* unknown window, or shape <= 0 after defaults     */
+  BNFFT_E_SPECTRAL_FACTOR_VANISHES = -6, /* |psi^_1(k)| < 1e-12 |psi^_1(0)|          */
+  BNFFT_E_NODE_NOT_FINITE = -7,          /* a coordinate is NaN or +-Inf                     */
+  BNFFT_E_NODE_OUT_OF_RANGE = -8,        /* a coordinate outside [-1/2, 1/2) (A5)            */
+  BNFFT_E_NODE_OUTSIDE_FEASIBLE_BOX = -9,/* STRICT_DOMAIN: outside [-1/2+m/L, 1/2-m/L]*/
+  BNFFT_E_NODES_NOT_SET = -10,           /* execute before a successful set_nodes            */
+  BNFFT_E_CUDA = -11,                    /* CUDA runtime error (incl. no device)             */
+  BNFFT_E_CUFFT = -12,                   /* cuFFT error                                      */
+  BNFFT_E_OOM = -13,                     /* device allocation failed                         */
+  BNFFT_E_UNSUPPORTED = -14,             /* parameters outside the compiled kernel set       */
+  BNFFT_E_INVALID_ARG = -15              /* NULL plan/pointer, n < 0, n >= 2^31, ...         */
+} bnfft_status;
+
+typedef enum { BNFFT_SINH = 0, BNFFT_GAUSS = 1, BNFFT_CKB = 2 } bnfft_window;
+typedef enum { BNFFT_C64 = 0, BNFFT_C128 = 1 } bnfft_prec;
+
+enum {
+  BNFFT_STRICT_DOMAIN = 1u,  /* reject nodes outside the closed feasible box   */
+  BNFFT_TIMING = 8u          /* record per-stage CUDA events (read with bnfft_get_timing)     */
+};
+
+/* Plan options.  d: 1..3.  M: even >= 2.  sigma >= 1, L = 2 ceil(ceil(sigma M)/2).
+ * m: truncation parameter, 1 <= m, 2m < L; compiled range m <= 16 (d=1), 12 (d=2), 8 (d=3).
+ * window: bnfft_window.  shape: beta (sinh, cKB) or s in x units (Gaussian); <= 0 selects the
+ * default of readings A1/A2.  prec: arithmetic of steps 1-3 (C64: fp32 complex64 grid and
+ * taps; C128: fp64).  Nodes are always float64.  batch >= 1 spectra share one node set.
+ * flags: BNFFT_STRICT_DOMAIN | BNFFT_TIMING.  device: CUDA ordinal.  stream: cudaStream_t
+ * (NULL = legacy default stream) on which every kernel and copy of this plan is issued. */
+typedef struct {
+  int32_t d;
+  int64_t M;
+  double sigma;
+  int32_t m;
+  int32_t window;
+  double shape;
+  int32_t prec;
+  int32_t batch;
+  uint32_t flags;
+  int32_t device;
+  void* stream;
+} bnfft_opts;
+
+/* Plan description.  Node binning geometry (for the stable bin sort, row a1): the cell of
+ * a node is c_t = floor(L x_t) + L/2 in [0, L) (clamped to L-1), its bin b_t = c_t >> bin_log2[t],
+ * and its sort key is the row-major bin index (dim 0 slowest) over bins_per_dim. */
+typedef struct {
+  int32_t d;
+  int64_t M;
+  int64_t L;
+  int32_t m;
+  int32_t window;
+  double shape;
+  int32_t prec;
+  int32_t batch;
+  int32_t bin_log2[3];
+  int64_t bins_per_dim[3];
+  int64_t nbins;
+  int32_t key_bits;
+  int32_t sort_passes;
+  double flatness;          /* max_k |L psi^_1(k) - 1| on I_M                    */
+  int64_t n_nodes;          /* nodes of the last successful set_nodes (0 if none)          */
+  int64_t grid_bytes;       /* bytes of one theta grid (batch x L^d complex)               */
+  int64_t device_bytes;     /* device memory currently owned by the plan                   */
+} bnfft_info;
+
+/* Per-stage device times (ms) accumulated since the last reset, and call counts.  Only
+ * recorded with BNFFT_TIMING.  Events are recorded on the plan's stream around each stage's
+ * kernels; reading them synchronizes with those events. */
+typedef struct {
+  double ms_psihat, ms_keys, ms_sort, ms_build, ms_deconv, ms_fft, ms_gather;
+  int64_t n_psihat, n_set_nodes, n_execute;
+  int64_t kernel_launches;  /* this library's own kernels launched (cuFFT not counted)    */
+} bnfft_timing;
+
+/* Create a plan: validates options, allocates device buffers, creates the cuFFT plan and runs
+ * step 0(a) (bnfft_precompute).  Synchronous.  On error *out is NULL. */
+BNFFT_API int bnfft_plan_create(const bnfft_opts* opts, struct bnfft_plan_s** out);
+
+/* Algorithm 2 step 0(a): psi^_1(k), k in I_M, by quadrature on the device, and the
+ * folded deconvolution factors q(k) = (-1)^k / (L psi^_1(k)) (A8, A9).  Stream-ordered,
+ * asynchronous; plan_create calls it and checks the result. */
+BNFFT_API int bnfft_precompute(struct bnfft_plan_s* plan);
+
+/* Set the node set.  x_dev: device pointer, n x d float64, row-major, user order; may be freed
+ * after return (the plan keeps a sorted copy).  n in [0, 2^31).  Validates every node (finite,
+ * in [-1/2, 1/2)^d, and the feasible box with STRICT_DOMAIN), then sorts the nodes stably by bin
+ * (row a1).  Synchronous (reads back the validation result).  On a bad node returns the code of
+ * the lowest offending index and stores that index in *first_bad (if non-NULL; else -1). */
+BNFFT_API int bnfft_set_nodes(struct bnfft_plan_s* plan, int64_t n, const double* x_dev, int64_t* first_bad);
+
+/* Steps 1-3.  fhat_dev: device, batch x M^d complex (complex64 for C64, complex128 for C128;
+ * interleaved re/im), centred row-major (index k_t + M/2, last dim fastest), batch slowest.
+ * f_dev: device, batch x n complex of the same precision, user node order.  Stream-ordered and
+ * asynchronous; errors of earlier asynchronous work surface as BNFFT_E_CUDA. */
+BNFFT_API int bnfft_execute(struct bnfft_plan_s* plan, const void* fhat_dev, void* f_dev);
+
+/* End-to-end helper with HOST buffers: copies x (n x d float64) and f^ host->device, runs
+ * set_nodes and execute, copies f device->host, and synchronizes.  Pinned host memory gives
+ * asynchronous DMA; pageable memory works but is staged by the CUDA driver. */
+BNFFT_API int bnfft_transform_host(struct bnfft_plan_s* plan, int64_t n, const double* x_host,
+                         const void* fhat_host, void* f_host, int64_t* first_bad);
+
+BNFFT_API int bnfft_get_info(const struct bnfft_plan_s* plan, bnfft_info* out);
+BNFFT_API int bnfft_get_timing(struct bnfft_plan_s* plan, bnfft_timing* out);
+BNFFT_API int bnfft_reset_timing(struct bnfft_plan_s* plan);
+
+/* Stage outputs for parity checks (synchronous copies):
+ *   bnfft_get_psihat: M float64 values psi^_1(k), k = -M/2..M/2-1, into host memory.
+ *   bnfft_get_grid:   the theta grid of the last execute (batch x L^d complex, centred index
+ *                     l_t + L/2, row-major) into a device buffer of grid_bytes.
+ *   bnfft_get_perm:   n uint32: sorted position -> user index, into a device buffer.
+ *   bnfft_get_bin_offsets: nbins+1 uint32: first sorted position of each bin, into a device buffer. */
+BNFFT_API int bnfft_get_psihat(const struct bnfft_plan_s* plan, double* host_out);
+BNFFT_API int bnfft_get_grid(const struct bnfft_plan_s* plan, void* dev_out);
+BNFFT_API int bnfft_get_perm(const struct bnfft_plan_s* plan, uint32_t* dev_out);
+BNFFT_API int bnfft_get_bin_offsets(const struct bnfft_plan_s* plan, uint32_t* dev_out);
+
+/* Release every resource of the plan (after synchronizing its stream).  NULL is a no-op. */
+BNFFT_API int bnfft_destroy(struct bnfft_plan_s* plan);
+
+BNFFT_API const char* bnfft_status_string(int status);
+BNFFT_API const char* bnfft_last_error(void);
+/* Library version and the compiled target ("sm_100a"). */
+BNFFT_API const char* bnfft_build_info(void);
+
+typedef struct bnfft_plan_s* bnfft_plan;
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BNFFT_H */

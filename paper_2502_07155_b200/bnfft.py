@@ -1,0 +1,212 @@
+"""Thin Python binding of the bnfft C ABI (include/bnfft.h) -- argument marshalling only.
+
+Every computation happens in libbnfft.so's CUDA kernels (and cuFFT for step 2).  There is no
+Python or CPU fallback: importing this module without the built library raises ImportError,
+and creating a plan without a CUDA device raises BnfftError(BNFFT_E_CUDA).
+
+Functions with the C names (bnfft_plan_create, bnfft_set_nodes, ...) return the raw status
+code; `Plan` wraps them for torch tensors (device memory, the current CUDA stream).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint32, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbnfft.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2502_07155_b200.build` "
+                      "(there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ----------------------------------------------------------------------------- constants
+BNFFT_OK = 0
+STATUS = {
+    0: "BNFFT_OK", -1: "BNFFT_E_BAD_DIM", -2: "BNFFT_E_BAD_BANDWIDTH", -3: "BNFFT_E_BAD_SIGMA",
+    -4: "BNFFT_E_TRUNCATION_TOO_LARGE", -5: "BNFFT_E_BAD_WINDOW_PARAM",
+    -6: "BNFFT_E_SPECTRAL_FACTOR_VANISHES", -7: "BNFFT_E_NODE_NOT_FINITE",
+    -8: "BNFFT_E_NODE_OUT_OF_RANGE", -9: "BNFFT_E_NODE_OUTSIDE_FEASIBLE_BOX",
+    -10: "BNFFT_E_NODES_NOT_SET", -11: "BNFFT_E_CUDA", -12: "BNFFT_E_CUFFT", -13: "BNFFT_E_OOM",
+    -14: "BNFFT_E_UNSUPPORTED", -15: "BNFFT_E_INVALID_ARG",
+}
+globals().update({v: k for k, v in STATUS.items()})
+BNFFT_SINH, BNFFT_GAUSS, BNFFT_CKB = 0, 1, 2
+BNFFT_C64, BNFFT_C128 = 0, 1
+BNFFT_STRICT_DOMAIN = 1
+BNFFT_TIMING = 8
+WINDOWS = {"sinh": BNFFT_SINH, "gauss": BNFFT_GAUSS, "ckb": BNFFT_CKB}
+PRECS = {"c64": BNFFT_C64, "c128": BNFFT_C128}
+
+
+class bnfft_opts(ctypes.Structure):
+    _fields_ = [("d", c_int32), ("M", c_int64), ("sigma", c_double), ("m", c_int32),
+                ("window", c_int32), ("shape", c_double), ("prec", c_int32), ("batch", c_int32),
+                ("flags", c_uint32), ("device", c_int32), ("stream", c_void_p)]
+
+
+class bnfft_info(ctypes.Structure):
+    _fields_ = [("d", c_int32), ("M", c_int64), ("L", c_int64), ("m", c_int32),
+                ("window", c_int32), ("shape", c_double), ("prec", c_int32), ("batch", c_int32),
+                ("bin_log2", c_int32 * 3), ("bins_per_dim", c_int64 * 3), ("nbins", c_int64),
+                ("key_bits", c_int32), ("sort_passes", c_int32), ("flatness", c_double),
+                ("n_nodes", c_int64), ("grid_bytes", c_int64), ("device_bytes", c_int64)]
+
+
+class bnfft_timing(ctypes.Structure):
+    _fields_ = [("ms_psihat", c_double), ("ms_keys", c_double), ("ms_sort", c_double),
+                ("ms_build", c_double), ("ms_deconv", c_double), ("ms_fft", c_double),
+                ("ms_gather", c_double), ("n_psihat", c_int64), ("n_set_nodes", c_int64),
+                ("n_execute", c_int64), ("kernel_launches", c_int64)]
+
+
+_P = c_void_p
+_sig = {
+    "bnfft_plan_create": (c_int, [POINTER(bnfft_opts), POINTER(c_void_p)]),
+    "bnfft_precompute": (c_int, [_P]),
+    "bnfft_set_nodes": (c_int, [_P, c_int64, c_void_p, POINTER(c_int64)]),
+    "bnfft_execute": (c_int, [_P, c_void_p, c_void_p]),
+    "bnfft_transform_host": (c_int, [_P, c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_int64)]),
+    "bnfft_get_info": (c_int, [_P, POINTER(bnfft_info)]),
+    "bnfft_get_timing": (c_int, [_P, POINTER(bnfft_timing)]),
+    "bnfft_reset_timing": (c_int, [_P]),
+    "bnfft_get_psihat": (c_int, [_P, c_void_p]),
+    "bnfft_get_grid": (c_int, [_P, c_void_p]),
+    "bnfft_get_perm": (c_int, [_P, c_void_p]),
+    "bnfft_get_bin_offsets": (c_int, [_P, c_void_p]),
+    "bnfft_destroy": (c_int, [_P]),
+    "bnfft_status_string": (c_char_p, [c_int]),
+    "bnfft_last_error": (c_char_p, []),
+    "bnfft_build_info": (c_char_p, []),
+}
+EXPORTED = tuple(_sig)
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+    globals()[_name] = _f
+
+
+class BnfftError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        detail = _lib.bnfft_last_error().decode(errors="replace")
+        super().__init__(f"{what}: {STATUS.get(code, code)} ({detail})")
+
+
+def check(code: int, what: str = "") -> None:
+    if code != BNFFT_OK:
+        raise BnfftError(code, what)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else (t if isinstance(t, int) else t.data_ptr())
+
+
+class Plan:
+    """Owning handle of a bnfft plan on one CUDA device (torch tensors for buffers)."""
+
+    def __init__(self, d: int, M: int, sigma: float, m: int, window: str = "sinh",
+                 prec: str = "c128", batch: int = 1, shape: float = 0.0, strict: bool = False,
+                 timing: bool = False, device: int = 0, stream: int | None = None):
+        import torch
+        self._torch = torch
+        if stream is None:
+            with torch.cuda.device(device):
+                stream = torch.cuda.current_stream(device).cuda_stream
+        o = bnfft_opts(d=d, M=M, sigma=sigma, m=m, window=WINDOWS[window], shape=shape,
+                       prec=PRECS[prec], batch=batch,
+                       flags=(BNFFT_STRICT_DOMAIN if strict else 0) | (BNFFT_TIMING if timing else 0),
+                       device=device, stream=stream)
+        h = c_void_p()
+        check(bnfft_plan_create(ctypes.byref(o), ctypes.byref(h)), "bnfft_plan_create")
+        self.h = h
+        self.d, self.M, self.m, self.batch, self.prec, self.device = d, M, m, batch, prec, device
+        self.cdtype = torch.complex128 if prec == "c128" else torch.complex64
+        self.n = 0
+
+    # -- C calls
+    def precompute(self) -> None:
+        check(bnfft_precompute(self.h), "bnfft_precompute")
+
+    def set_nodes(self, x) -> None:
+        t = self._torch
+        assert x.dtype == t.float64 and x.is_cuda and x.is_contiguous()
+        n = x.shape[0]
+        bad = c_int64(-1)
+        code = bnfft_set_nodes(self.h, n, _ptr(x) if n else None, ctypes.byref(bad))
+        if code != BNFFT_OK:
+            err = BnfftError(code, "bnfft_set_nodes")
+            err.first_bad = bad.value
+            raise err
+        self.n = n
+
+    def execute(self, fhat, out=None):
+        t = self._torch
+        assert fhat.dtype == self.cdtype and fhat.is_cuda and fhat.is_contiguous()
+        assert fhat.numel() == self.batch * self.M ** self.d
+        if out is None:
+            out = t.empty((self.batch, self.n), dtype=self.cdtype, device=fhat.device)
+        check(bnfft_execute(self.h, _ptr(fhat), _ptr(out) if self.n else None), "bnfft_execute")
+        return out
+
+    def transform_host(self, x_host, fhat_host, f_host) -> None:
+        bad = c_int64(-1)
+        check(bnfft_transform_host(self.h, x_host.shape[0], _ptr(x_host), _ptr(fhat_host),
+                                   _ptr(f_host), ctypes.byref(bad)), "bnfft_transform_host")
+
+    def info(self) -> bnfft_info:
+        i = bnfft_info()
+        check(bnfft_get_info(self.h, ctypes.byref(i)), "bnfft_get_info")
+        return i
+
+    def timing(self) -> bnfft_timing:
+        tm = bnfft_timing()
+        check(bnfft_get_timing(self.h, ctypes.byref(tm)), "bnfft_get_timing")
+        return tm
+
+    def reset_timing(self) -> None:
+        check(bnfft_reset_timing(self.h), "bnfft_reset_timing")
+
+    def psihat(self):
+        import numpy as np
+        a = np.empty(self.M, dtype=np.float64)
+        check(bnfft_get_psihat(self.h, a.ctypes.data), "bnfft_get_psihat")
+        return a
+
+    def grid(self):
+        t = self._torch
+        i = self.info()
+        g = t.empty((self.batch,) + (i.L,) * self.d, dtype=self.cdtype, device=f"cuda:{self.device}")
+        check(bnfft_get_grid(self.h, _ptr(g)), "bnfft_get_grid")
+        return g
+
+    def perm(self):
+        t = self._torch
+        p = t.empty(max(self.n, 1), dtype=t.int32, device=f"cuda:{self.device}")
+        check(bnfft_get_perm(self.h, _ptr(p)), "bnfft_get_perm")
+        return p[: self.n]
+
+    def bin_offsets(self):
+        t = self._torch
+        i = self.info()
+        o = t.empty(i.nbins + 1, dtype=t.int32, device=f"cuda:{self.device}")
+        check(bnfft_get_bin_offsets(self.h, _ptr(o)), "bnfft_get_bin_offsets")
+        return o
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            bnfft_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

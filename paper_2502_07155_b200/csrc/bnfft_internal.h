@@ -1,0 +1,144 @@
+// Internal declarations of the bnfft library (product path).  Shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/bnfft.h"
+
+namespace bnfft {
+
+constexpr int kGatherThreads = 256;   // nodes per gather CTA chunk (one node per thread)
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;        // keys per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kMaxDigitBits = 8;
+constexpr int kQuadN = 64;            // Gauss-Legendre points for psi^ (reading A4)
+
+// Window parameters in grid units tau = L x (|tau| <= m is the support).
+struct WinParams {
+  int window;        // bnfft_window
+  int m;
+  double inv_m;      // 1/m
+  double beta;       // sinh / cKB shape
+  double inv_norm;   // 1/sinh(beta) or 1/(I0(beta)-1)
+  double gauss_b;    // Gaussian: phi(tau/L) = exp(-gauss_b tau^2), gauss_b = 1/(2 s^2 L^2)
+  float beta_f, inv_norm_f, gauss_b_f, inv_m_f;
+};
+
+// phi(tau/L) (eq. varphisinh; cKB P:302-310; Gaussian reading A2), fp64.
+__device__ __forceinline__ double phi_tau_d(double tau, const WinParams& w) {
+  double t = tau * w.inv_m;
+  if (fabs(t) > 1.0) return 0.0;
+  double r = (1.0 - t) * (1.0 + t);
+  if (w.window == BNFFT_SINH) return sinh(w.beta * sqrt(r)) * w.inv_norm;
+  if (w.window == BNFFT_CKB) return (cyl_bessel_i0(w.beta * sqrt(r)) - 1.0) * w.inv_norm;
+  return exp(-w.gauss_b * tau * tau);
+}
+
+// fp32 variant used by the complex64 path.
+__device__ __forceinline__ float phi_tau_f(float tau, const WinParams& w) {
+  float t = tau * w.inv_m_f;
+  if (fabsf(t) > 1.0f) return 0.0f;
+  float r = (1.0f - t) * (1.0f + t);
+  if (w.window == BNFFT_SINH) {
+    float a = w.beta_f * sqrtf(r);
+    float e = expf(a);
+    return 0.5f * (e - 1.0f / e) * w.inv_norm_f;
+  }
+  if (w.window == BNFFT_CKB) return (cyl_bessel_i0f(w.beta_f * sqrtf(r)) - 1.0f) * w.inv_norm_f;
+  return expf(-w.gauss_b_f * tau * tau);
+}
+
+struct Timer {
+  int stage;
+  cudaEvent_t a, b;
+};
+
+enum Stage { ST_PSIHAT = 0, ST_KEYS, ST_SORT, ST_BUILD, ST_DECONV, ST_FFT, ST_GATHER, ST_COUNT };
+
+}  // namespace bnfft
+
+struct bnfft_plan_s {
+  bnfft_opts opts;
+  int64_t L = 0, Ld = 0, Md = 0;
+  double shape = 0;
+  bnfft::WinParams wp{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool c128 = false;
+  size_t csize = 8;  // bytes per complex
+
+  // binning
+  int bin_log2[3] = {0, 0, 0};
+  int64_t nb_dim[3] = {1, 1, 1};
+  int64_t nbins = 1;
+  int key_bits = 0, sort_passes = 0, digit_bits = 0;
+
+  // plan-owned device buffers
+  double* d_gl = nullptr;       // 2*kQuadN: theta_q, weights
+  double* d_psihat = nullptr;   // M
+  double* d_q = nullptr;        // M
+  double* d_flat = nullptr;     // 2 doubles: flatness, min|psihat|/|psihat(0)|
+  void* d_fft_in = nullptr;     // batch x L^d complex, zero outside I_M (set once)
+  void* d_grid = nullptr;       // batch x L^d complex, theta (centred)
+  cufftHandle fft = 0;
+  bool fft_ok = false;
+  double flatness = 0;
+
+  // nodes
+  int64_t n = 0, cap = 0;
+  bool nodes_set = false;
+  double* d_xs = nullptr;        // sorted nodes n x d
+  uint32_t* d_perm = nullptr;    // sorted pos -> user index
+  uint32_t* d_skeys = nullptr;   // sorted keys (points into keys buffers)
+  uint32_t* d_bin_start = nullptr;  // nbins + 1
+  uint32_t *d_k0 = nullptr, *d_k1 = nullptr, *d_v0 = nullptr, *d_v1 = nullptr;
+  uint32_t* d_hist = nullptr;    // digits x tiles
+  uint32_t* d_scan_part = nullptr;
+  int64_t hist_cap = 0, part_cap = 0;
+  unsigned long long* d_bad = nullptr;   // (index << 4) | code
+  unsigned long long* h_bad = nullptr;   // pinned
+
+  // host transform staging
+  double* d_x_stage = nullptr; int64_t x_stage_cap = 0;
+  void* d_fhat_stage = nullptr;
+  void* d_f_stage = nullptr; int64_t f_stage_cap = 0;
+
+  int gather_bt = 1;          // batch slice per staged box
+  size_t gather_smem = 0;
+
+  // timing
+  std::vector<bnfft::Timer> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[bnfft::ST_COUNT] = {0};
+  int64_t n_psihat = 0, n_set = 0, n_exec = 0, launches = 0;
+  int64_t device_bytes = 0;
+};
+
+namespace bnfft {
+
+// error helpers (plan.cu)
+void set_error(const std::string& s);
+int cuda_fail(cudaError_t e, const char* what);
+
+// timing helpers
+void timer_begin(bnfft_plan_s* p, int stage, cudaEvent_t* ev);
+void timer_end(bnfft_plan_s* p, int stage, cudaEvent_t ev);
+
+// launchers
+cudaError_t launch_psihat(bnfft_plan_s* p);
+cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n);
+cudaError_t launch_sort(bnfft_plan_s* p, int64_t n);
+cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n);
+cudaError_t launch_deconv(bnfft_plan_s* p, const void* fhat);
+cudaError_t launch_gather(bnfft_plan_s* p, void* out);
+int gather_supported(int d, int m);
+size_t gather_box_elems(const bnfft_plan_s* p);
+cudaError_t gather_prepare(bnfft_plan_s* p);
+
+}  // namespace bnfft

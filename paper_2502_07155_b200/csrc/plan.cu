@@ -1,0 +1,584 @@
+// Host orchestration of the C ABI declared in include/bnfft.h: option validation (readings
+// A1, A2, A7), device buffers, cuFFT plan, stage sequencing and per-stage CUDA-event timing.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "bnfft_internal.h"
+
+using namespace bnfft;
+
+namespace bnfft {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& s) { g_err = s; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  if (e == cudaErrorMemoryAllocation) return BNFFT_E_OOM;
+  return BNFFT_E_CUDA;
+}
+
+static cudaEvent_t get_event(bnfft_plan_s* p) {
+  if (!p->pool.empty()) {
+    cudaEvent_t e = p->pool.back();
+    p->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void timer_begin(bnfft_plan_s* p, int stage, cudaEvent_t* ev) {
+  (void)stage;
+  *ev = nullptr;
+  if (!(p->opts.flags & BNFFT_TIMING)) return;
+  *ev = get_event(p);
+  cudaEventRecord(*ev, p->stream);
+}
+
+void timer_end(bnfft_plan_s* p, int stage, cudaEvent_t ev) {
+  if (!(p->opts.flags & BNFFT_TIMING) || !ev) return;
+  cudaEvent_t b = get_event(p);
+  cudaEventRecord(b, p->stream);
+  p->pending.push_back(Timer{stage, ev, b});
+}
+
+// Gauss-Legendre nodes/weights on [-1, 1] by Newton iteration on the three-term recurrence of
+// P_n (long double), mapped to theta in [0, pi/2] (reading A4).  Independent of numpy.
+static void gauss_legendre_theta(int n, double* theta, double* w) {
+  const long double PI = 3.141592653589793238462643383279502884L;
+  for (int i = 0; i < n; ++i) {
+    long double x = cosl(PI * (i + 0.75L) / (n + 0.5L));
+    long double dp = 0;
+    for (int it = 0; it < 100; ++it) {
+      long double p0 = 1, p1 = x;
+      for (int k = 2; k <= n; ++k) {
+        long double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1);
+      long double dx = p1 / dp;
+      x -= dx;
+      if (fabsl(dx) < 1e-19L) break;
+    }
+    {
+      long double p0 = 1, p1 = x;
+      for (int k = 2; k <= n; ++k) {
+        long double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1);
+    }
+    long double wi = 2 / ((1 - x * x) * dp * dp);
+    theta[i] = (double)((x + 1) * (PI / 4));
+    w[i] = (double)(wi * (PI / 4));
+  }
+}
+
+static int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+static int ceil_log2(int64_t v) {
+  int b = 0;
+  while (((int64_t)1 << b) < v) ++b;
+  return b;
+}
+
+template <typename T>
+static cudaError_t dmalloc(bnfft_plan_s* p, T** ptr, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc((void**)ptr, bytes);
+  if (e == cudaSuccess) p->device_bytes += (int64_t)bytes;
+  return e;
+}
+
+static void dfree(void* ptr) {
+  if (ptr) cudaFree(ptr);
+}
+
+static int collect_timing(bnfft_plan_s* p) {
+  for (auto& t : p->pending) {
+    cudaError_t e = cudaEventSynchronize(t.b);
+    if (e != cudaSuccess) return cuda_fail(e, "timing event");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    p->ms[t.stage] += ms;
+    p->pool.push_back(t.a);
+    p->pool.push_back(t.b);
+  }
+  p->pending.clear();
+  return BNFFT_OK;
+}
+
+static void free_nodes(bnfft_plan_s* p) {
+  dfree(p->d_xs);
+  dfree(p->d_k0);
+  dfree(p->d_k1);
+  dfree(p->d_v0);
+  dfree(p->d_v1);
+  p->d_xs = nullptr;
+  p->d_k0 = p->d_k1 = p->d_v0 = p->d_v1 = nullptr;
+  p->d_perm = p->d_skeys = nullptr;
+  p->cap = 0;
+}
+
+}  // namespace bnfft
+
+extern "C" {
+
+const char* bnfft_status_string(int s) {
+  switch (s) {
+    case BNFFT_OK: return "ok";
+    case BNFFT_E_BAD_DIM: return "bad dimension";
+    case BNFFT_E_BAD_BANDWIDTH: return "bad bandwidth (M must be even and >= 2)";
+    case BNFFT_E_BAD_SIGMA: return "bad oversampling factor (sigma >= 1)";
+    case BNFFT_E_TRUNCATION_TOO_LARGE: return "truncation parameter out of range (1 <= m, 2m < L)";
+    case BNFFT_E_BAD_WINDOW_PARAM: return "bad window or window parameter";
+    case BNFFT_E_SPECTRAL_FACTOR_VANISHES: return "psi^ vanishes in band";
+    case BNFFT_E_NODE_NOT_FINITE: return "node not finite";
+    case BNFFT_E_NODE_OUT_OF_RANGE: return "node outside [-1/2, 1/2)^d";
+    case BNFFT_E_NODE_OUTSIDE_FEASIBLE_BOX: return "node outside the feasible box";
+    case BNFFT_E_NODES_NOT_SET: return "nodes not set";
+    case BNFFT_E_CUDA: return "CUDA error";
+    case BNFFT_E_CUFFT: return "cuFFT error";
+    case BNFFT_E_OOM: return "out of device memory";
+    case BNFFT_E_UNSUPPORTED: return "unsupported parameters";
+    case BNFFT_E_INVALID_ARG: return "invalid argument";
+    default: return "unknown status";
+  }
+}
+
+const char* bnfft_last_error(void) { return g_err.c_str(); }
+
+const char* bnfft_build_info(void) {
+  return "bnfft 0.1 (arXiv 2502.07155 Algorithm 2), target sm_100a";
+}
+
+int bnfft_destroy(bnfft_plan_s* p) {
+  if (!p) return BNFFT_OK;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  else cudaDeviceSynchronize();
+  if (p->fft_ok) cufftDestroy(p->fft);
+  dfree(p->d_gl);
+  dfree(p->d_psihat);
+  dfree(p->d_q);
+  dfree(p->d_flat);
+  dfree(p->d_fft_in);
+  dfree(p->d_grid);
+  dfree(p->d_bin_start);
+  dfree(p->d_hist);
+  dfree(p->d_scan_part);
+  dfree(p->d_bad);
+  dfree(p->d_x_stage);
+  dfree(p->d_fhat_stage);
+  dfree(p->d_f_stage);
+  free_nodes(p);
+  if (p->h_bad) cudaFreeHost(p->h_bad);
+  for (auto& t : p->pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : p->pool) cudaEventDestroy(e);
+  delete p;
+  return BNFFT_OK;
+}
+
+int bnfft_precompute(bnfft_plan_s* p) {
+  if (!p) return BNFFT_E_INVALID_ARG;
+  cudaEvent_t ev;
+  timer_begin(p, ST_PSIHAT, &ev);
+  cudaError_t e = launch_psihat(p);
+  if (e != cudaSuccess) return cuda_fail(e, "psihat kernel");
+  timer_end(p, ST_PSIHAT, ev);
+  p->n_psihat++;
+  return BNFFT_OK;
+}
+
+int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
+  if (!out) return BNFFT_E_INVALID_ARG;
+  *out = nullptr;
+  if (!o) return BNFFT_E_INVALID_ARG;
+  if (o->d < 1 || o->d > 3) { set_error("d must be 1..3"); return BNFFT_E_BAD_DIM; }
+  if (o->M < 2 || (o->M & 1)) { set_error("M must be even and >= 2 (P:50)"); return BNFFT_E_BAD_BANDWIDTH; }
+  if (!std::isfinite(o->sigma) || o->sigma < 1.0) { set_error("sigma >= 1 (P:86)"); return BNFFT_E_BAD_SIGMA; }
+  // L = M_sigma = 2 ceil(ceil(sigma M)/2) (reading A7)
+  double sm = std::ceil(o->sigma * (double)o->M);
+  int64_t L = 2 * (int64_t)std::ceil(sm / 2.0);
+  if (o->m < 1 || 2 * (int64_t)o->m >= L) { set_error("need 1 <= m and 2m < L"); return BNFFT_E_TRUNCATION_TOO_LARGE; }
+  if (o->window != BNFFT_SINH && o->window != BNFFT_GAUSS && o->window != BNFFT_CKB) {
+    set_error("unknown window");
+    return BNFFT_E_BAD_WINDOW_PARAM;
+  }
+  if (o->prec != BNFFT_C64 && o->prec != BNFFT_C128) { set_error("prec"); return BNFFT_E_INVALID_ARG; }
+  if (o->batch < 1) { set_error("batch >= 1"); return BNFFT_E_INVALID_ARG; }
+  if (!gather_supported(o->d, o->m)) { set_error("m outside the compiled range for this d"); return BNFFT_E_UNSUPPORTED; }
+  double shape = o->shape;
+  if (!(shape > 0)) {
+    if (o->window == BNFFT_GAUSS) {
+      if (L == o->M) { set_error("Gaussian default s needs L > M (reading A2)"); return BNFFT_E_BAD_WINDOW_PARAM; }
+      shape = std::sqrt((double)o->m / (M_PI * (double)L * (double)(L - o->M)));  // A2
+    } else {
+      shape = M_PI * o->m * (1.0 - (double)o->M / (double)L);                        // A1
+    }
+  }
+  if (!(shape > 0) || !std::isfinite(shape)) { set_error("window shape must be > 0"); return BNFFT_E_BAD_WINDOW_PARAM; }
+  int64_t Ld = ipow(L, o->d), Md = ipow(o->M, o->d);
+  if (Ld > ((int64_t)1 << 34)) { set_error("grid too large"); return BNFFT_E_UNSUPPORTED; }
+
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0) {
+    set_error(std::string("no CUDA device: ") + cudaGetErrorString(ce));
+    return BNFFT_E_CUDA;
+  }
+  ce = cudaSetDevice(o->device);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
+
+  bnfft_plan_s* p = new bnfft_plan_s();
+  p->opts = *o;
+  p->device = o->device;
+  p->stream = (cudaStream_t)o->stream;
+  p->L = L;
+  p->Ld = Ld;
+  p->Md = Md;
+  p->shape = shape;
+  p->c128 = o->prec == BNFFT_C128;
+  p->csize = p->c128 ? 16 : 8;
+
+  WinParams& w = p->wp;
+  w.window = o->window;
+  w.m = o->m;
+  w.inv_m = 1.0 / o->m;
+  w.inv_m_f = (float)w.inv_m;
+  w.beta = shape;
+  w.beta_f = (float)shape;
+  if (o->window == BNFFT_SINH) w.inv_norm = 1.0 / std::sinh(shape);
+  else if (o->window == BNFFT_CKB) w.inv_norm = 1.0 / (std::cyl_bessel_i(0.0, shape) - 1.0);
+  else w.inv_norm = 1.0;
+  w.inv_norm_f = (float)w.inv_norm;
+  w.gauss_b = (o->window == BNFFT_GAUSS) ? 1.0 / (2.0 * shape * shape * (double)L * (double)L) : 0.0;
+  w.gauss_b_f = (float)w.gauss_b;
+  if (!std::isfinite(w.inv_norm) || w.inv_norm <= 0) {
+    delete p;
+    set_error("window normalisation overflow (shape too large)");
+    return BNFFT_E_BAD_WINDOW_PARAM;
+  }
+
+  // node binning geometry (row a1)
+  int lg = 7;
+  if (o->d == 2) lg = 4;
+  if (o->d == 3) lg = o->batch > 1 ? 2 : 3;
+  int lgL = 0;
+  while (((int64_t)1 << (lgL + 1)) <= L) ++lgL;
+  lg = std::min(lg, lgL);
+  int64_t nbins = 1;
+  for (int t = 0; t < 3; ++t) {
+    p->bin_log2[t] = t < o->d ? lg : 0;
+    p->nb_dim[t] = t < o->d ? (L + (1 << lg) - 1) >> lg : 1;
+    nbins *= p->nb_dim[t];
+  }
+  p->nbins = nbins;
+  p->key_bits = ceil_log2(nbins);
+  p->sort_passes = (p->key_bits + kMaxDigitBits - 1) / kMaxDigitBits;
+  p->digit_bits = p->sort_passes ? (p->key_bits + p->sort_passes - 1) / p->sort_passes : 0;
+
+  int rc = BNFFT_OK;
+  cudaError_t e;
+#define CK(call, what)                       \
+  do {                                       \
+    e = (call);                              \
+    if (e != cudaSuccess) {                  \
+      rc = cuda_fail(e, what);               \
+      goto fail;                             \
+    }                                        \
+  } while (0)
+  {
+    CK(dmalloc(p, &p->d_gl, 2 * kQuadN * sizeof(double)), "alloc gl");
+    CK(dmalloc(p, &p->d_psihat, o->M * sizeof(double)), "alloc psihat");
+    CK(dmalloc(p, &p->d_q, o->M * sizeof(double)), "alloc q");
+    CK(dmalloc(p, &p->d_flat, 2 * sizeof(double)), "alloc flat");
+    size_t gbytes = (size_t)Ld * o->batch * p->csize;
+    CK(dmalloc(p, &p->d_fft_in, gbytes), "alloc fft input");
+    CK(dmalloc(p, &p->d_grid, gbytes), "alloc grid");
+    CK(dmalloc(p, &p->d_bin_start, (nbins + 1) * sizeof(uint32_t)), "alloc bin offsets");
+    CK(dmalloc(p, &p->d_bad, sizeof(unsigned long long)), "alloc status");
+    CK(cudaMallocHost((void**)&p->h_bad, sizeof(unsigned long long)), "alloc pinned status");
+    CK(cudaMemsetAsync(p->d_fft_in, 0, gbytes, p->stream), "zero fft input");
+    CK(cudaMemsetAsync(p->d_grid, 0, gbytes, p->stream), "zero grid");
+    double th[2 * kQuadN];
+    gauss_legendre_theta(kQuadN, th, th + kQuadN);
+    CK(cudaMemcpyAsync(p->d_gl, th, sizeof(th), cudaMemcpyHostToDevice, p->stream), "copy gl");
+    CK(gather_prepare(p), "gather kernel attributes");
+
+    int n[3] = {(int)L, (int)L, (int)L};
+    size_t ws = 0;
+    cufftResult fr = cufftCreate(&p->fft);
+    if (fr == CUFFT_SUCCESS) {
+      p->fft_ok = true;
+      fr = cufftMakePlanMany(p->fft, o->d, n, nullptr, 1, (int)Ld, nullptr, 1, (int)Ld,
+                             p->c128 ? CUFFT_Z2Z : CUFFT_C2C, o->batch, &ws);
+    }
+    if (fr == CUFFT_SUCCESS) fr = cufftSetStream(p->fft, p->stream);
+    if (fr != CUFFT_SUCCESS) {
+      char buf[96];
+      snprintf(buf, sizeof(buf), "cuFFT plan failed (%d)", (int)fr);
+      set_error(buf);
+      rc = BNFFT_E_CUFFT;
+      goto fail;
+    }
+    p->device_bytes += (int64_t)ws;
+
+    rc = bnfft_precompute(p);
+    if (rc != BNFFT_OK) goto fail;
+    double fl[2];
+    CK(cudaMemcpyAsync(fl, p->d_flat, sizeof(fl), cudaMemcpyDeviceToHost, p->stream), "copy flat");
+    CK(cudaStreamSynchronize(p->stream), "plan sync");
+    p->flatness = fl[0];
+    if (!(fl[1] >= 1e-12)) {
+      set_error("|psi^_1(k)| < 1e-12 |psi^_1(0)| for some k in I_M (P:429)");
+      rc = BNFFT_E_SPECTRAL_FACTOR_VANISHES;
+      goto fail;
+    }
+  }
+#undef CK
+  *out = p;
+  return BNFFT_OK;
+fail:
+  bnfft_destroy(p);
+  return rc;
+}
+
+int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad) {
+  if (first_bad) *first_bad = -1;
+  if (!p) return BNFFT_E_INVALID_ARG;
+  if (n < 0 || n >= ((int64_t)1 << 31) || (n > 0 && !x)) {
+    set_error("n must be in [0, 2^31) and x non-NULL");
+    return BNFFT_E_INVALID_ARG;
+  }
+  cudaSetDevice(p->device);
+  p->nodes_set = false;
+  cudaError_t e;
+  if (n > p->cap) {
+    free_nodes(p);
+    int64_t cap = std::max<int64_t>(n, 1);
+    size_t b4 = cap * sizeof(uint32_t);
+    if ((e = dmalloc(p, &p->d_xs, cap * p->opts.d * sizeof(double))) != cudaSuccess ||
+        (e = dmalloc(p, &p->d_k0, b4)) != cudaSuccess || (e = dmalloc(p, &p->d_k1, b4)) != cudaSuccess ||
+        (e = dmalloc(p, &p->d_v0, b4)) != cudaSuccess || (e = dmalloc(p, &p->d_v1, b4)) != cudaSuccess)
+      return cuda_fail(e, "alloc nodes");
+    p->cap = cap;
+  }
+  int64_t ntiles = (std::max<int64_t>(n, 1) + kSortTile - 1) / kSortTile;
+  int64_t nh = ((int64_t)1 << std::max(p->digit_bits, 1)) * ntiles;
+  if (nh > p->hist_cap) {
+    dfree(p->d_hist);
+    p->d_hist = nullptr;
+    if ((e = dmalloc(p, &p->d_hist, nh * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "alloc hist");
+    p->hist_cap = nh;
+  }
+  int64_t np = (nh + 4095) / 4096 + 1;
+  if (np > p->part_cap) {
+    dfree(p->d_scan_part);
+    p->d_scan_part = nullptr;
+    if ((e = dmalloc(p, &p->d_scan_part, np * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "alloc scan");
+    p->part_cap = np;
+  }
+
+  cudaEvent_t ev;
+  timer_begin(p, ST_KEYS, &ev);
+  if ((e = launch_keys(p, x, n)) != cudaSuccess) return cuda_fail(e, "keys kernel");
+  timer_end(p, ST_KEYS, ev);
+  if ((e = cudaMemcpyAsync(p->h_bad, p->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           p->stream)) != cudaSuccess)
+    return cuda_fail(e, "status copy");
+  timer_begin(p, ST_SORT, &ev);
+  if ((e = launch_sort(p, n)) != cudaSuccess) return cuda_fail(e, "sort kernels");
+  timer_end(p, ST_SORT, ev);
+  timer_begin(p, ST_BUILD, &ev);
+  if ((e = launch_build(p, x, n)) != cudaSuccess) return cuda_fail(e, "build kernel");
+  timer_end(p, ST_BUILD, ev);
+  if ((e = cudaStreamSynchronize(p->stream)) != cudaSuccess) return cuda_fail(e, "set_nodes sync");
+  unsigned long long bad = *p->h_bad;
+  if (bad != ~0ull) {
+    int64_t idx = (int64_t)(bad >> 4);
+    int code = (int)(bad & 15);
+    if (first_bad) *first_bad = idx;
+    char buf[128];
+    snprintf(buf, sizeof(buf), "node %lld rejected", (long long)idx);
+    set_error(buf);
+    p->n = 0;
+    if (code == 1) return BNFFT_E_NODE_NOT_FINITE;
+    if (code == 2) return BNFFT_E_NODE_OUT_OF_RANGE;
+    return BNFFT_E_NODE_OUTSIDE_FEASIBLE_BOX;
+  }
+  p->n = n;
+  p->nodes_set = true;
+  p->n_set++;
+  return BNFFT_OK;
+}
+
+int bnfft_execute(bnfft_plan_s* p, const void* fhat, void* f) {
+  if (!p) return BNFFT_E_INVALID_ARG;
+  if (!p->nodes_set) { set_error("call bnfft_set_nodes first"); return BNFFT_E_NODES_NOT_SET; }
+  if (!fhat || (p->n > 0 && !f)) { set_error("NULL buffer"); return BNFFT_E_INVALID_ARG; }
+  cudaSetDevice(p->device);
+  cudaError_t e;
+  cudaEvent_t ev;
+  timer_begin(p, ST_DECONV, &ev);
+  if ((e = launch_deconv(p, fhat)) != cudaSuccess) return cuda_fail(e, "deconv kernel");
+  timer_end(p, ST_DECONV, ev);
+  timer_begin(p, ST_FFT, &ev);
+  cufftResult fr = p->c128 ? cufftExecZ2Z(p->fft, (cufftDoubleComplex*)p->d_fft_in,
+                                          (cufftDoubleComplex*)p->d_grid, CUFFT_INVERSE)
+                           : cufftExecC2C(p->fft, (cufftComplex*)p->d_fft_in,
+                                          (cufftComplex*)p->d_grid, CUFFT_INVERSE);
+  if (fr != CUFFT_SUCCESS) {
+    char buf[64];
+    snprintf(buf, sizeof(buf), "cufftExec failed (%d)", (int)fr);
+    set_error(buf);
+    return BNFFT_E_CUFFT;
+  }
+  timer_end(p, ST_FFT, ev);
+  timer_begin(p, ST_GATHER, &ev);
+  if ((e = launch_gather(p, f)) != cudaSuccess) return cuda_fail(e, "gather kernel");
+  timer_end(p, ST_GATHER, ev);
+  p->n_exec++;
+  return BNFFT_OK;
+}
+
+int bnfft_transform_host(bnfft_plan_s* p, int64_t n, const double* x_host, const void* fhat_host,
+                         void* f_host, int64_t* first_bad) {
+  if (first_bad) *first_bad = -1;
+  if (!p || !fhat_host || (n > 0 && (!x_host || !f_host))) return BNFFT_E_INVALID_ARG;
+  if (n < 0 || n >= ((int64_t)1 << 31)) return BNFFT_E_INVALID_ARG;
+  cudaSetDevice(p->device);
+  cudaError_t e;
+  size_t xb = (size_t)n * p->opts.d * sizeof(double);
+  size_t fhb = (size_t)p->Md * p->opts.batch * p->csize;
+  size_t fb = (size_t)n * p->opts.batch * p->csize;
+  if (n > p->x_stage_cap) {
+    dfree(p->d_x_stage);
+    dfree(p->d_f_stage);
+    p->d_x_stage = nullptr;
+    p->d_f_stage = nullptr;
+    if ((e = dmalloc(p, &p->d_x_stage, xb)) != cudaSuccess) return cuda_fail(e, "alloc x stage");
+    if ((e = dmalloc(p, &p->d_f_stage, fb)) != cudaSuccess) return cuda_fail(e, "alloc f stage");
+    p->x_stage_cap = n;
+  }
+  if (!p->d_fhat_stage && (e = dmalloc(p, &p->d_fhat_stage, fhb)) != cudaSuccess)
+    return cuda_fail(e, "alloc fhat stage");
+  if (n > 0 && (e = cudaMemcpyAsync(p->d_x_stage, x_host, xb, cudaMemcpyHostToDevice, p->stream)) != cudaSuccess)
+    return cuda_fail(e, "H2D x");
+  if ((e = cudaMemcpyAsync(p->d_fhat_stage, fhat_host, fhb, cudaMemcpyHostToDevice, p->stream)) != cudaSuccess)
+    return cuda_fail(e, "H2D fhat");
+  int rc = bnfft_set_nodes(p, n, p->d_x_stage, first_bad);
+  if (rc != BNFFT_OK) return rc;
+  rc = bnfft_execute(p, p->d_fhat_stage, p->d_f_stage);
+  if (rc != BNFFT_OK) return rc;
+  if (n > 0 && (e = cudaMemcpyAsync(f_host, p->d_f_stage, fb, cudaMemcpyDeviceToHost, p->stream)) != cudaSuccess)
+    return cuda_fail(e, "D2H f");
+  if ((e = cudaStreamSynchronize(p->stream)) != cudaSuccess) return cuda_fail(e, "transform sync");
+  return BNFFT_OK;
+}
+
+int bnfft_get_info(const bnfft_plan_s* p, bnfft_info* o) {
+  if (!p || !o) return BNFFT_E_INVALID_ARG;
+  memset(o, 0, sizeof(*o));
+  o->d = p->opts.d;
+  o->M = p->opts.M;
+  o->L = p->L;
+  o->m = p->opts.m;
+  o->window = p->opts.window;
+  o->shape = p->shape;
+  o->prec = p->opts.prec;
+  o->batch = p->opts.batch;
+  for (int t = 0; t < 3; ++t) {
+    o->bin_log2[t] = p->bin_log2[t];
+    o->bins_per_dim[t] = p->nb_dim[t];
+  }
+  o->nbins = p->nbins;
+  o->key_bits = p->key_bits;
+  o->sort_passes = p->sort_passes;
+  o->flatness = p->flatness;
+  o->n_nodes = p->nodes_set ? p->n : 0;
+  o->grid_bytes = p->Ld * p->opts.batch * (int64_t)p->csize;
+  o->device_bytes = p->device_bytes;
+  return BNFFT_OK;
+}
+
+int bnfft_get_timing(bnfft_plan_s* p, bnfft_timing* o) {
+  if (!p || !o) return BNFFT_E_INVALID_ARG;
+  int rc = collect_timing(p);
+  if (rc != BNFFT_OK) return rc;
+  o->ms_psihat = p->ms[ST_PSIHAT];
+  o->ms_keys = p->ms[ST_KEYS];
+  o->ms_sort = p->ms[ST_SORT];
+  o->ms_build = p->ms[ST_BUILD];
+  o->ms_deconv = p->ms[ST_DECONV];
+  o->ms_fft = p->ms[ST_FFT];
+  o->ms_gather = p->ms[ST_GATHER];
+  o->n_psihat = p->n_psihat;
+  o->n_set_nodes = p->n_set;
+  o->n_execute = p->n_exec;
+  o->kernel_launches = p->launches;
+  return BNFFT_OK;
+}
+
+int bnfft_reset_timing(bnfft_plan_s* p) {
+  if (!p) return BNFFT_E_INVALID_ARG;
+  int rc = collect_timing(p);
+  for (int i = 0; i < ST_COUNT; ++i) p->ms[i] = 0;
+  p->n_psihat = p->n_set = p->n_exec = p->launches = 0;
+  return rc;
+}
+
+int bnfft_get_psihat(const bnfft_plan_s* p, double* host_out) {
+  if (!p || !host_out) return BNFFT_E_INVALID_ARG;
+  cudaSetDevice(p->device);
+  cudaError_t e = cudaMemcpyAsync(host_out, p->d_psihat, p->opts.M * sizeof(double),
+                                  cudaMemcpyDeviceToHost, p->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  return e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "get_psihat");
+}
+
+int bnfft_get_grid(const bnfft_plan_s* p, void* dev_out) {
+  if (!p || !dev_out) return BNFFT_E_INVALID_ARG;
+  cudaSetDevice(p->device);
+  cudaError_t e = cudaMemcpyAsync(dev_out, p->d_grid, (size_t)p->Ld * p->opts.batch * p->csize,
+                                  cudaMemcpyDeviceToDevice, p->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  return e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "get_grid");
+}
+
+int bnfft_get_perm(const bnfft_plan_s* p, uint32_t* dev_out) {
+  if (!p || !dev_out) return BNFFT_E_INVALID_ARG;
+  if (!p->nodes_set) return BNFFT_E_NODES_NOT_SET;
+  if (p->n == 0) return BNFFT_OK;
+  cudaSetDevice(p->device);
+  cudaError_t e = cudaMemcpyAsync(dev_out, p->d_perm, p->n * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToDevice, p->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  return e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "get_perm");
+}
+
+int bnfft_get_bin_offsets(const bnfft_plan_s* p, uint32_t* dev_out) {
+  if (!p || !dev_out) return BNFFT_E_INVALID_ARG;
+  if (!p->nodes_set) return BNFFT_E_NODES_NOT_SET;
+  cudaSetDevice(p->device);
+  cudaError_t e = cudaMemcpyAsync(dev_out, p->d_bin_start, (p->nbins + 1) * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToDevice, p->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  return e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "get_bin_offsets");
+}
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+// Row a1: node preprocessing (set_nodes).  Validation + bin keys (K1), stable LSD radix sort of
+// (key, user index) pairs (K2), sorted node copy and bin offsets (K3).  Hand-written, deterministic:
+// no atomics decide any position, so the permutation is bit-identical to a stable argsort of
+// the keys (reading A14: ties broken by the original index).
+//
+// Cell of a node (P:467-474 with reading A6): c_t = floor(L x_t), the grid point with l_t <= L x_t;
+// stored shifted to [0, L) as c_t + L/2.  L*x_t is one IEEE double product (__dmul_rn, never
+// contracted into an FMA).
+#include <algorithm>
+
+#include "bnfft_internal.h"
+
+namespace bnfft {
+
+struct KeyParams {
+  int d;
+  int64_t L;
+  double Lf;
+  int log2W[3];
+  int64_t nb[3];
+  int strict;
+  double box_lo, box_hi;
+};
+
+enum { BAD_NOT_FINITE = 1, BAD_RANGE = 2, BAD_BOX = 3 };
+
+// K1: validate + key.  bad = min over nodes of (index << 4 | code).
+__global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams kp,
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                            unsigned long long* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t key = 0;
+    int code = 0;
+    bool nonfinite = false, range = false, box = false;
+    for (int t = 0; t < kp.d; ++t) {
+      double xv = x[i * kp.d + t];
+      if (!isfinite(xv)) { nonfinite = true; continue; }
+      if (!(xv >= -0.5 && xv < 0.5)) { range = true; continue; }
+      if (kp.strict && !(xv >= kp.box_lo && xv <= kp.box_hi)) box = true;
+      double Lx = __dmul_rn(kp.Lf, xv);
+      int64_t c = (int64_t)floor(Lx) + kp.L / 2;
+      if (c > kp.L - 1) c = kp.L - 1;   // fl(L x) == L/2 for x < 1/2 (non-power-of-2 L only)
+      key = key * (uint32_t)kp.nb[t] + (uint32_t)(c >> kp.log2W[t]);
+    }
+    if (nonfinite) code = BAD_NOT_FINITE;
+    else if (range) code = BAD_RANGE;
+    else if (box) code = BAD_BOX;
+    if (code) {
+      atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)code);
+      key = 0;
+    }
+    keys[i] = key;
+    vals[i] = (uint32_t)i;
+  }
+}
+
+// K2a: per-tile digit histogram, stored digit-major: hist[digit * ntiles + tile].
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(
+    const uint32_t* __restrict__ keys, int64_t n, int shift, int bits,
+    uint32_t* __restrict__ hist, int64_t ntiles) {
+  __shared__ uint32_t cnt[1 << kMaxDigitBits];
+  const int ndig = 1 << bits;
+  const uint32_t mask = ndig - 1;
+  for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x) cnt[dgt] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll 4
+  for (int j = 0; j < kSortItems; ++j) {
+    int64_t idx = base + j * kSortThreads + threadIdx.x;
+    if (idx < n) atomicAdd(&cnt[(keys[idx] >> shift) & mask], 1u);   // integer counts: order-free
+  }
+  __syncthreads();
+  for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x)
+    hist[(int64_t)dgt * ntiles + blockIdx.x] = cnt[dgt];
+}
+
+// Exclusive scan of a uint32 array (3 phases).  Block = 256 threads x 16 items = 4096.
+constexpr int kScanItems = 16;
+constexpr int kScanBlock = 256 * kScanItems;
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t warp_sums[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = lane < 8 ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < 8) warp_sums[lane] = s;
+  }
+  __syncthreads();
+  uint32_t before = (w > 0 ? warp_sums[w - 1] : 0) + x - v;
+  *total = warp_sums[7];
+  __syncthreads();
+  return before;
+}
+
+__global__ void __launch_bounds__(256) scan_reduce_kernel(const uint32_t* __restrict__ in,
+                                                          int64_t n, uint32_t* __restrict__ part) {
+  const int64_t base = (int64_t)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j)
+    if (base + j < n) s += in[base + j];
+  uint32_t tot;
+  block_excl_scan(s, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256) scan_part_kernel(uint32_t* __restrict__ part, int64_t np) {
+  // single block; sequential over chunks of 256*kScanItems
+  uint32_t carry = 0;
+  for (int64_t c0 = 0; c0 < np; c0 += kScanBlock) {
+    const int64_t base = c0 + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      v[j] = (base + j < np) ? part[base + j] : 0;
+      s += v[j];
+    }
+    uint32_t tot;
+    uint32_t run = carry + block_excl_scan(s, &tot);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      if (base + j < np) part[base + j] = run;
+      run += v[j];
+    }
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(256) scan_down_kernel(const uint32_t* __restrict__ in, int64_t n,
+                                                        const uint32_t* __restrict__ part,
+                                                        uint32_t* __restrict__ out) {
+  const int64_t base = (int64_t)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    v[j] = (base + j < n) ? in[base + j] : 0;
+    s += v[j];
+  }
+  uint32_t tot;
+  uint32_t run = part[blockIdx.x] + block_excl_scan(s, &tot);
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    if (base + j < n) out[base + j] = run;
+    run += v[j];
+  }
+}
+
+// K2b: stable scatter.  Warp w of the CTA owns tile elements [w*512, (w+1)*512), visited in
+// 16 rounds of 32 consecutive elements; ranks within the warp come from warp-private digit
+// counters (match_any groups equal digits in a round, lower lanes first), ranks across warps
+// from an exclusive prefix over the warp counters, ranks across tiles from the scanned
+// digit-major histogram.  Element order inside the tile is therefore preserved.
+__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift, int bits,
+    const uint32_t* __restrict__ hist_scan, int64_t ntiles) {
+  constexpr int kWarps = kSortThreads / 32;
+  constexpr int kPerWarp = kSortTile / kWarps;   // 512
+  __shared__ uint32_t wcnt[kWarps][1 << kMaxDigitBits];
+  __shared__ uint32_t gbase[1 << kMaxDigitBits];
+  const int ndig = 1 << bits;
+  const uint32_t mask = ndig - 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kWarps * ndig; i += blockDim.x) wcnt[i / ndig][i % ndig] = 0;
+  for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x)
+    gbase[dgt] = hist_scan[(int64_t)dgt * ntiles + blockIdx.x];
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)w * kPerWarp;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t k[kSortItems], v[kSortItems], r[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    int64_t idx = base + j * 32 + lane;
+    bool valid = idx < n;
+    k[j] = valid ? kin[idx] : 0u;
+    v[j] = valid ? vin[idx] : 0u;
+    uint32_t dg = valid ? ((k[j] >> shift) & mask) : 0xffffffffu;
+    uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    uint32_t cnt = valid ? wcnt[w][dg] : 0u;
+    r[j] = cnt + __popc(peers & lt_mask);
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wcnt[w][dg] = cnt + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) {
+      uint32_t t = wcnt[ww][dgt];
+      wcnt[ww][dgt] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    int64_t idx = base + j * 32 + lane;
+    if (idx < n) {
+      uint32_t dg = (k[j] >> shift) & mask;
+      uint32_t pos = gbase[dg] + wcnt[w][dg] + r[j];
+      kout[pos] = k[j];
+      vout[pos] = v[j];
+    }
+  }
+}
+
+// K3: sorted node copy xs[i] = x[perm[i]] and bin offsets from the sorted keys.
+__global__ void build_kernel(const double* __restrict__ x, const uint32_t* __restrict__ perm,
+                             const uint32_t* __restrict__ skeys, double* __restrict__ xs,
+                             uint32_t* __restrict__ bin_start, int64_t n, int d, int64_t nbins) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) {
+      uint32_t j = perm[i];
+      for (int t = 0; t < d; ++t) xs[i * d + t] = x[(int64_t)j * d + t];
+    }
+    int64_t kprev = (i == 0) ? -1 : (int64_t)skeys[i - 1];
+    int64_t kcur = (i == n) ? nbins : (int64_t)skeys[i];
+    for (int64_t b = kprev + 1; b <= kcur; ++b) bin_start[b] = (uint32_t)i;
+  }
+}
+
+static int grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148LL * 32));
+}
+
+cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
+  KeyParams kp;
+  kp.d = p->opts.d;
+  kp.L = p->L;
+  kp.Lf = (double)p->L;
+  for (int t = 0; t < 3; ++t) {
+    kp.log2W[t] = p->bin_log2[t];
+    kp.nb[t] = p->nb_dim[t];
+  }
+  kp.strict = (p->opts.flags & BNFFT_STRICT_DOMAIN) ? 1 : 0;
+  kp.box_lo = -0.5 + (double)p->opts.m / (double)p->L;
+  kp.box_hi = 0.5 - (double)p->opts.m / (double)p->L;
+  cudaError_t e = cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), p->stream);
+  if (e != cudaSuccess) return e;
+  if (n > 0) {
+    keys_kernel<<<grid_for(n, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0, p->d_v0, p->d_bad);
+    p->launches++;
+  }
+  return cudaGetLastError();
+}
+
+static cudaError_t exclusive_scan(bnfft_plan_s* p, const uint32_t* in, uint32_t* out, int64_t n) {
+  int64_t nb = (n + kScanBlock - 1) / kScanBlock;
+  scan_reduce_kernel<<<(unsigned)nb, 256, 0, p->stream>>>(in, n, p->d_scan_part);
+  scan_part_kernel<<<1, 256, 0, p->stream>>>(p->d_scan_part, nb);
+  scan_down_kernel<<<(unsigned)nb, 256, 0, p->stream>>>(in, n, p->d_scan_part, out);
+  p->launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
+  uint32_t *kin = p->d_k0, *vin = p->d_v0, *kout = p->d_k1, *vout = p->d_v1;
+  if (n > 0 && p->sort_passes > 0) {
+    int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+    int bits = p->digit_bits;
+    for (int pass = 0; pass < p->sort_passes; ++pass) {
+      int shift = pass * bits;
+      int b = std::min(bits, p->key_bits - shift);
+      int64_t nh = ((int64_t)1 << b) * ntiles;
+      radix_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, p->stream>>>(kin, n, shift, b,
+                                                                          p->d_hist, ntiles);
+      p->launches++;
+      cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
+      if (e != cudaSuccess) return e;
+      radix_scatter_kernel<<<(unsigned)ntiles, kSortThreads, 0, p->stream>>>(
+          kin, vin, kout, vout, n, shift, b, p->d_hist, ntiles);
+      p->launches++;
+      std::swap(kin, kout);
+      std::swap(vin, vout);
+    }
+  }
+  p->d_skeys = kin;
+  p->d_perm = vin;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n) {
+  build_kernel<<<grid_for(n + 1, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys, p->d_xs,
+                                                            p->d_bin_start, n, p->opts.d,
+                                                            p->nbins);
+  p->launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace bnfft
