@@ -69,7 +69,8 @@ typedef enum { BNFFT_C64 = 0, BNFFT_C128 = 1 } bnfft_prec;
 
 enum {
   BNFFT_STRICT_DOMAIN = 1u,  /* reject nodes outside the closed feasible box   */
-  BNFFT_TIMING = 8u          /* record per-stage CUDA events (read with bnfft_get_timing)     */
+  BNFFT_TIMING = 8u,         /* record per-stage CUDA events (read with bnfft_get_timing)     */
+  BNFFT_EXACT_TAPS = 16u     /* gather evaluates sinc * phi directly (no tap polynomials)       */
 };
 
 /* Plan options.  d: 1..3.  M: even >= 2.  sigma >= 1, L = 2 ceil(ceil(sigma M)/2).
@@ -77,7 +78,7 @@ enum {
  * window: bnfft_window.  shape: beta (sinh, cKB) or s in x units (Gaussian); <= 0 selects the
  * default of readings A1/A2.  prec: arithmetic of steps 1-3 (C64: fp32 complex64 grid and
  * taps; C128: fp64).  Nodes are always float64.  batch >= 1 spectra share one node set.
- * flags: BNFFT_STRICT_DOMAIN | BNFFT_TIMING.  device: CUDA ordinal.  stream: cudaStream_t
+ * flags: BNFFT_STRICT_DOMAIN | BNFFT_TIMING | BNFFT_EXACT_TAPS.  device: CUDA ordinal.  stream: cudaStream_t
  * (NULL = legacy default stream) on which every kernel and copy of this plan is issued. */
 typedef struct {
   int32_t d;
@@ -95,7 +96,11 @@ typedef struct {
 
 /* Plan description.  Node binning geometry (for the stable bin sort, row a1): the cell of
  * a node is c_t = floor(L x_t) + L/2 in [0, L) (clamped to L-1), its bin b_t = c_t >> bin_log2[t],
- * and its sort key is the row-major bin index (dim 0 slowest) over bins_per_dim. */
+ * its bin index is row-major (dim 0 slowest) over bins_per_dim, and its sort key is
+ * (j >> user_block_log2) * nbins + bin for user index j.  Nodes are sorted stably by that key
+ * (ties by user index); nkeys = ceil(n / 2^user_block_log2) * nbins for the current node set.
+ * tap_poly: the gather evaluates psi by per-tap polynomials (fit error tap_fit_err, checked at
+ * plan creation) rather than by direct sinc * phi evaluation. */
 typedef struct {
   int32_t d;
   int64_t M;
@@ -108,6 +113,10 @@ typedef struct {
   int32_t bin_log2[3];
   int64_t bins_per_dim[3];
   int64_t nbins;
+  int32_t user_block_log2;
+  int64_t nkeys;
+  int32_t tap_poly;
+  double tap_fit_err;
   int32_t key_bits;
   int32_t sort_passes;
   double flatness;          /* max_k |L psi^_1(k) - 1| on I_M                    */
@@ -162,7 +171,8 @@ BNFFT_API int bnfft_reset_timing(struct bnfft_plan_s* plan);
  *   bnfft_get_grid:   the theta grid of the last execute (batch x L^d complex, centred index
  *                     l_t + L/2, row-major) into a device buffer of grid_bytes.
  *   bnfft_get_perm:   n uint32: sorted position -> user index, into a device buffer.
- *   bnfft_get_bin_offsets: nbins+1 uint32: first sorted position of each bin, into a device buffer. */
+ *   bnfft_get_bin_offsets: nkeys+1 uint32: first sorted position of each sort key (user block,
+ *                     bin), into a device buffer. */
 BNFFT_API int bnfft_get_psihat(const struct bnfft_plan_s* plan, double* host_out);
 BNFFT_API int bnfft_get_grid(const struct bnfft_plan_s* plan, void* dev_out);
 BNFFT_API int bnfft_get_perm(const struct bnfft_plan_s* plan, uint32_t* dev_out);

@@ -35,6 +35,7 @@ BNFFT_SINH, BNFFT_GAUSS, BNFFT_CKB = 0, 1, 2
 BNFFT_C64, BNFFT_C128 = 0, 1
 BNFFT_STRICT_DOMAIN = 1
 BNFFT_TIMING = 8
+BNFFT_EXACT_TAPS = 16
 WINDOWS = {"sinh": BNFFT_SINH, "gauss": BNFFT_GAUSS, "ckb": BNFFT_CKB}
 PRECS = {"c64": BNFFT_C64, "c128": BNFFT_C128}
 
@@ -49,7 +50,8 @@ class bnfft_info(ctypes.Structure):
     _fields_ = [("d", c_int32), ("M", c_int64), ("L", c_int64), ("m", c_int32),
                 ("window", c_int32), ("shape", c_double), ("prec", c_int32), ("batch", c_int32),
                 ("bin_log2", c_int32 * 3), ("bins_per_dim", c_int64 * 3), ("nbins", c_int64),
-                ("key_bits", c_int32), ("sort_passes", c_int32), ("flatness", c_double),
+                ("user_block_log2", c_int32), ("nkeys", c_int64), ("tap_poly", c_int32),
+                ("tap_fit_err", c_double), ("key_bits", c_int32), ("sort_passes", c_int32), ("flatness", c_double),
                 ("n_nodes", c_int64), ("grid_bytes", c_int64), ("device_bytes", c_int64)]
 
 
@@ -108,7 +110,8 @@ class Plan:
 
     def __init__(self, d: int, M: int, sigma: float, m: int, window: str = "sinh",
                  prec: str = "c128", batch: int = 1, shape: float = 0.0, strict: bool = False,
-                 timing: bool = False, device: int = 0, stream: int | None = None):
+                 timing: bool = False, exact_taps: bool = False, device: int = 0,
+                 stream: int | None = None):
         import torch
         self._torch = torch
         if stream is None:
@@ -116,7 +119,8 @@ class Plan:
                 stream = torch.cuda.current_stream(device).cuda_stream
         o = bnfft_opts(d=d, M=M, sigma=sigma, m=m, window=WINDOWS[window], shape=shape,
                        prec=PRECS[prec], batch=batch,
-                       flags=(BNFFT_STRICT_DOMAIN if strict else 0) | (BNFFT_TIMING if timing else 0),
+                       flags=(BNFFT_STRICT_DOMAIN if strict else 0) | (BNFFT_TIMING if timing else 0)
+                       | (BNFFT_EXACT_TAPS if exact_taps else 0),
                        device=device, stream=stream)
         h = c_void_p()
         check(bnfft_plan_create(ctypes.byref(o), ctypes.byref(h)), "bnfft_plan_create")
@@ -190,7 +194,7 @@ class Plan:
     def bin_offsets(self):
         t = self._torch
         i = self.info()
-        o = t.empty(i.nbins + 1, dtype=t.int32, device=f"cuda:{self.device}")
+        o = t.empty(i.nkeys + 1, dtype=t.int32, device=f"cuda:{self.device}")
         check(bnfft_get_bin_offsets(self.h, _ptr(o)), "bnfft_get_bin_offsets")
         return o
 

@@ -78,6 +78,15 @@ struct bnfft_plan_s {
   int64_t nb_dim[3] = {1, 1, 1};
   int64_t nbins = 1;
   int key_bits = 0, sort_passes = 0, digit_bits = 0;
+  int ub_log2 = 31;            // user-block size of the sort key (user block, bin); 31 = one block
+  int64_t nkeys = 1;           // number of (user block, bin) keys of the current node set
+  int64_t key_start_cap = 0;
+
+  // gather tap polynomials (plan time, tapfit kernel)
+  bool tap_poly = true;
+  int tap_nc = 0;              // coefficients per tap
+  double tap_fit_err = 0;      // max |poly - exact| over taps (plan-time check)
+  std::vector<double> tap_coef;   // T x tap_nc, monomials in x = 2u - 1
 
   // plan-owned device buffers
   double* d_gl = nullptr;       // 2*kQuadN: theta_q, weights
@@ -96,7 +105,7 @@ struct bnfft_plan_s {
   double* d_xs = nullptr;        // sorted nodes n x d
   uint32_t* d_perm = nullptr;    // sorted pos -> user index
   uint32_t* d_skeys = nullptr;   // sorted keys (points into keys buffers)
-  uint32_t* d_bin_start = nullptr;  // nbins + 1
+  uint32_t* d_bin_start = nullptr;  // nkeys + 1: first sorted position of each (user block, bin)
   uint32_t *d_k0 = nullptr, *d_k1 = nullptr, *d_v0 = nullptr, *d_v1 = nullptr;
   uint32_t* d_hist = nullptr;    // digits x tiles
   uint32_t* d_scan_part = nullptr;
@@ -110,6 +119,8 @@ struct bnfft_plan_s {
   void* d_f_stage = nullptr; int64_t f_stage_cap = 0;
 
   int gather_bt = 1;          // batch slice per staged box
+  int gather_smax = 1;        // segments (bins) staged per round
+  int gather_box_cap = 0;     // d = 1: staged window capacity (complex elements)
   size_t gather_smem = 0;
 
   // timing
@@ -132,6 +143,7 @@ void timer_end(bnfft_plan_s* p, int stage, cudaEvent_t ev);
 
 // launchers
 cudaError_t launch_psihat(bnfft_plan_s* p);
+cudaError_t launch_tapfit(bnfft_plan_s* p, int NC, double* d_coef, double* d_err);
 cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n);
 cudaError_t launch_sort(bnfft_plan_s* p, int64_t n);
 cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n);
@@ -140,5 +152,6 @@ cudaError_t launch_gather(bnfft_plan_s* p, void* out);
 int gather_supported(int d, int m);
 size_t gather_box_elems(const bnfft_plan_s* p);
 cudaError_t gather_prepare(bnfft_plan_s* p);
+int tap_coef_count(bool c128);
 
 }  // namespace bnfft

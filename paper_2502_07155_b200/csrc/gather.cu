@@ -1,12 +1,14 @@
 // Row a6 gather: host-side dispatch and launch (kernels in gather_impl.cuh).
+#include <cstring>
+
 #include "gather_impl.cuh"
 
 namespace bnfft {
 
-static const void* select_kernel(int d, int m, bool c128) {
-  if (d == 1) return c128 ? gather_kernel_1d(m) : gather_kernel_1f(m);
-  if (d == 2) return c128 ? gather_kernel_2d(m) : gather_kernel_2f(m);
-  if (d == 3) return c128 ? gather_kernel_3d(m) : gather_kernel_3f(m);
+static const void* select_kernel(int d, int m, bool c128, bool poly) {
+  if (d == 1) return c128 ? gather_kernel_1d(m, poly) : gather_kernel_1f(m, poly);
+  if (d == 2) return c128 ? gather_kernel_2d(m, poly) : gather_kernel_2f(m, poly);
+  if (d == 3) return c128 ? gather_kernel_3d(m, poly) : gather_kernel_3f(m, poly);
   return nullptr;
 }
 
@@ -24,29 +26,41 @@ size_t gather_box_elems(const bnfft_plan_s* p) {
   return e;
 }
 
+// Dynamic shared memory for staged boxes; the kernel also uses ~2 KB of static shared memory, and
+// the sum must stay under the 48 KB default (the attribute is raised only for single large boxes).
+static size_t smem_budget() { return 40u << 10; }
+constexpr int kMaxSegPerRound = 32;
+
 cudaError_t gather_prepare(bnfft_plan_s* p) {
-  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128);
+  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly);
   if (!fn) return cudaErrorInvalidValue;
-  size_t per = gather_box_elems(p) * p->csize;
-  int bt = (int)std::max<size_t>(1, std::min<size_t>((size_t)p->opts.batch, (48u << 10) / per));
-  p->gather_bt = bt;
-  p->gather_smem = per * bt;
-  if (p->gather_smem > (48u << 10)) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)p->gather_smem);
-    if (e != cudaSuccess) return e;
+  if (p->opts.d == 1) {
+    // one contiguous window per CTA chunk; capacity 32 KB
+    p->gather_box_cap = (int)((32u << 10) / p->csize);
+    p->gather_smem = (size_t)p->gather_box_cap * p->csize;
+    p->gather_bt = 1;
+    p->gather_smax = 1;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
   }
+  size_t per = gather_box_elems(p) * p->csize;
+  int bt = (int)std::max<size_t>(1, std::min<size_t>((size_t)p->opts.batch, smem_budget() / per));
+  p->gather_bt = bt;
+  int smax = (int)std::max<size_t>(1, std::min<size_t>(kMaxSegPerRound, smem_budget() / (per * bt)));
+  p->gather_smax = smax;
+  p->gather_smem = per * bt * smax;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(p->gather_smem, 1));
+  if (e != cudaSuccess) return e;
   return cudaSuccess;
 }
 
-cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
-  if (p->n == 0) return cudaSuccess;
-  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128);
-  if (!fn) return cudaErrorInvalidValue;
-  GatherParams gp;
+template <typename R>
+static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
+  static_assert(sizeof(GatherParams<R>) < 32000, "kernel parameter limit");
+  GatherParams<R> gp;
+  memset(&gp, 0, sizeof(gp));
   gp.xs = p->d_xs;
   gp.perm = p->d_perm;
-  gp.bin_start = p->d_bin_start;
   gp.grid = p->d_grid;
   gp.out = out;
   gp.n = p->n;
@@ -55,19 +69,39 @@ cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
   gp.Lf = (double)p->L;
   gp.batch = p->opts.batch;
   gp.bt = p->gather_bt;
+  gp.smax = p->gather_smax;
   for (int t = 0; t < 3; ++t) {
     gp.log2W[t] = p->bin_log2[t];
     gp.nb[t] = p->nb_dim[t];
     gp.box[t] = t < p->opts.d ? (1 << p->bin_log2[t]) + 2 * p->opts.m - 1 : 1;
   }
   gp.box_elems = (int)gather_box_elems(p);
+  gp.edge_sqrt = p->opts.window == BNFFT_SINH ? 1 : 0;
+  gp.inv_m = (R)(1.0 / p->opts.m);
   gp.wp = p->wp;
+  gp.boxcap = p->gather_box_cap;
+  constexpr int NC = PolyN<R>::NC;
+  if (p->tap_poly) {
+    const int T = 2 * p->opts.m;
+    for (int i = 0; i < T; ++i)
+      for (int k = 0; k < NC; ++k) gp.coef[k][i] = (R)p->tap_coef[(size_t)i * NC + k];
+  }
   void* args[] = {&gp};
-  unsigned blocks = (unsigned)((p->n + kGatherThreads - 1) / kGatherThreads);
+  const int64_t per_cta = p->opts.d == 1 ? (int64_t)kGatherThreads * kNPT1 : kGatherThreads;
+  unsigned blocks = (unsigned)((p->n + per_cta - 1) / per_cta);
   cudaError_t e = cudaLaunchKernel(fn, dim3(blocks), dim3(kGatherThreads), args, p->gather_smem,
                                    p->stream);
   p->launches++;
   return e;
 }
+
+cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
+  if (p->n == 0) return cudaSuccess;
+  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly);
+  if (!fn) return cudaErrorInvalidValue;
+  return p->c128 ? launch_gather_t<double>(p, out, fn) : launch_gather_t<float>(p, out, fn);
+}
+
+int tap_coef_count(bool c128) { return c128 ? PolyN<double>::NC : PolyN<float>::NC; }
 
 }  // namespace bnfft

@@ -1,6 +1,8 @@
-// Instantiation unit: gather kernels for d = 1, float arithmetic.
+// Dispatch for d = 1, float: polynomial-tap or exact-tap kernels.
 #include "gather_impl.cuh"
 
 namespace bnfft {
-const void* gather_kernel_1f(int m) { return kernel_for<1, float, kMaxM1>(m); }
+const void* gather_kernel_1f_p(int m);
+const void* gather_kernel_1f_e(int m);
+const void* gather_kernel_1f(int m, bool poly) { return poly ? gather_kernel_1f_p(m) : gather_kernel_1f_e(m); }
 }  // namespace bnfft

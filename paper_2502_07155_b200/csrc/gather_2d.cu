@@ -1,6 +1,8 @@
-// Instantiation unit: gather kernels for d = 2, double arithmetic.
+// Dispatch for d = 2, double: polynomial-tap or exact-tap kernels.
 #include "gather_impl.cuh"
 
 namespace bnfft {
-const void* gather_kernel_2d(int m) { return kernel_for<2, double, kMaxM2>(m); }
+const void* gather_kernel_2d_p(int m);
+const void* gather_kernel_2d_e(int m);
+const void* gather_kernel_2d(int m, bool poly) { return poly ? gather_kernel_2d_p(m) : gather_kernel_2d_e(m); }
 }  // namespace bnfft

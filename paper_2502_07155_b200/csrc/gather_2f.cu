@@ -1,6 +1,8 @@
-// Instantiation unit: gather kernels for d = 2, float arithmetic.
+// Dispatch for d = 2, float: polynomial-tap or exact-tap kernels.
 #include "gather_impl.cuh"
 
 namespace bnfft {
-const void* gather_kernel_2f(int m) { return kernel_for<2, float, kMaxM2>(m); }
+const void* gather_kernel_2f_p(int m);
+const void* gather_kernel_2f_e(int m);
+const void* gather_kernel_2f(int m, bool poly) { return poly ? gather_kernel_2f_p(m) : gather_kernel_2f_e(m); }
 }  // namespace bnfft

@@ -291,6 +291,20 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   p->key_bits = ceil_log2(nbins);
   p->sort_passes = (p->key_bits + kMaxDigitBits - 1) / kMaxDigitBits;
   p->digit_bits = p->sort_passes ? (p->key_bits + p->sort_passes - 1) / p->sort_passes : 0;
+  // Sort key (user block, bin), row a1: for d <= 2 (grid resident in L2) nodes are binned inside
+  // user blocks whose outputs (batch x csize each) span ~16 MiB, so the gather's writes to
+  // f[perm[i]] stay within an L2-resident window; d = 3 uses one block (grid reuse dominates).
+  {
+    int64_t gbytes_one = Ld * (int64_t)o->batch * (int64_t)p->csize;
+    if (o->d <= 2 && gbytes_one <= ((int64_t)48 << 20)) {
+      int64_t per = (int64_t)o->batch * (int64_t)p->csize;
+      int ub = 12;
+      while (ub < 31 && (((int64_t)1 << (ub + 1)) * per) <= ((int64_t)16 << 20)) ++ub;
+      p->ub_log2 = ub;
+    } else {
+      p->ub_log2 = 31;
+    }
+  }
 
   int rc = BNFFT_OK;
   cudaError_t e;
@@ -310,7 +324,6 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     size_t gbytes = (size_t)Ld * o->batch * p->csize;
     CK(dmalloc(p, &p->d_fft_in, gbytes), "alloc fft input");
     CK(dmalloc(p, &p->d_grid, gbytes), "alloc grid");
-    CK(dmalloc(p, &p->d_bin_start, (nbins + 1) * sizeof(uint32_t)), "alloc bin offsets");
     CK(dmalloc(p, &p->d_bad, sizeof(unsigned long long)), "alloc status");
     CK(cudaMallocHost((void**)&p->h_bad, sizeof(unsigned long long)), "alloc pinned status");
     CK(cudaMemsetAsync(p->d_fft_in, 0, gbytes, p->stream), "zero fft input");
@@ -318,6 +331,33 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     double th[2 * kQuadN];
     gauss_legendre_theta(kQuadN, th, th + kQuadN);
     CK(cudaMemcpyAsync(p->d_gl, th, sizeof(th), cudaMemcpyHostToDevice, p->stream), "copy gl");
+    {
+      // tap polynomials of the gather (row a6): fit + accuracy check on the device
+      const int T = 2 * o->m;
+      const int NC = tap_coef_count(p->c128);
+      double *d_coef = nullptr, *d_err = nullptr;
+      CK(cudaMalloc((void**)&d_coef, (size_t)T * NC * sizeof(double)), "alloc tap coef");
+      e = cudaMalloc((void**)&d_err, (size_t)T * sizeof(double));
+      if (e == cudaSuccess) e = launch_tapfit(p, NC, d_coef, d_err);
+      p->tap_coef.assign((size_t)T * NC, 0.0);
+      std::vector<double> err(T, 0.0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(p->tap_coef.data(), d_coef, (size_t)T * NC * sizeof(double),
+                            cudaMemcpyDeviceToHost, p->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(err.data(), d_err, (size_t)T * sizeof(double), cudaMemcpyDeviceToHost,
+                            p->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+      cudaFree(d_coef);
+      if (d_err) cudaFree(d_err);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "tap fit"); goto fail; }
+      double mx = 0;
+      for (double v : err) mx = std::max(mx, v);
+      p->tap_fit_err = mx;
+      p->tap_nc = NC;
+      p->tap_poly = std::isfinite(mx) && mx <= (p->c128 ? 1e-13 : 2e-6) &&
+                    !(o->flags & BNFFT_EXACT_TAPS);
+    }
     CK(gather_prepare(p), "gather kernel attributes");
 
     int n[3] = {(int)L, (int)L, (int)L};
@@ -394,6 +434,17 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
     p->part_cap = np;
   }
 
+  {
+    int64_t nblk = n > 0 ? ((n - 1) >> p->ub_log2) + 1 : 1;
+    p->nkeys = nblk * p->nbins;
+    if (p->nkeys + 1 > p->key_start_cap) {
+      dfree(p->d_bin_start);
+      p->d_bin_start = nullptr;
+      if ((e = dmalloc(p, &p->d_bin_start, (p->nkeys + 1) * sizeof(uint32_t))) != cudaSuccess)
+        return cuda_fail(e, "alloc key offsets");
+      p->key_start_cap = p->nkeys + 1;
+    }
+  }
   cudaEvent_t ev;
   timer_begin(p, ST_KEYS, &ev);
   if ((e = launch_keys(p, x, n)) != cudaSuccess) return cuda_fail(e, "keys kernel");
@@ -507,6 +558,10 @@ int bnfft_get_info(const bnfft_plan_s* p, bnfft_info* o) {
     o->bins_per_dim[t] = p->nb_dim[t];
   }
   o->nbins = p->nbins;
+  o->user_block_log2 = p->ub_log2;
+  o->nkeys = p->nkeys;
+  o->tap_poly = p->tap_poly ? 1 : 0;
+  o->tap_fit_err = p->tap_fit_err;
   o->key_bits = p->key_bits;
   o->sort_passes = p->sort_passes;
   o->flatness = p->flatness;
@@ -575,7 +630,7 @@ int bnfft_get_bin_offsets(const bnfft_plan_s* p, uint32_t* dev_out) {
   if (!p || !dev_out) return BNFFT_E_INVALID_ARG;
   if (!p->nodes_set) return BNFFT_E_NODES_NOT_SET;
   cudaSetDevice(p->device);
-  cudaError_t e = cudaMemcpyAsync(dev_out, p->d_bin_start, (p->nbins + 1) * sizeof(uint32_t),
+  cudaError_t e = cudaMemcpyAsync(dev_out, p->d_bin_start, (p->nkeys + 1) * sizeof(uint32_t),
                                   cudaMemcpyDeviceToDevice, p->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
   return e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "get_bin_offsets");

@@ -28,6 +28,8 @@ enum { BAD_NOT_FINITE = 1, BAD_RANGE = 2, BAD_BOX = 3 };
 __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams kp,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                             unsigned long long* __restrict__ bad) {
+  // vals (identity permutation) is only written when no radix pass will run; the first pass
+  // generates v = index itself.
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t key = 0;
@@ -51,14 +53,29 @@ __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams k
       key = 0;
     }
     keys[i] = key;
-    vals[i] = (uint32_t)i;
+    if (vals) vals[i] = (uint32_t)i;
   }
 }
 
-// K2a: per-tile digit histogram, stored digit-major: hist[digit * ntiles + tile].
+// Sort key = (user block, bin): the input is in user order, so the user-block part of the key is
+// already sorted; the radix passes run over the bin digits only, with the per-tile histograms laid
+// out block-major so that the scan never moves an element across a user block:
+//   hist[blk*tpb*ndig + dg*tiles_in(blk) + tile_in_blk]      (scan order = (blk, digit, tile)).
+struct SegLayout {
+  int64_t tpb;      // tiles per user block
+  int64_t ntiles;
+};
+__device__ __forceinline__ int64_t hist_index(const SegLayout& sl, int64_t tile, int dg, int ndig) {
+  const int64_t blk = tile / sl.tpb;
+  const int64_t tib = tile - blk * sl.tpb;
+  const int64_t tin = min(sl.tpb, sl.ntiles - blk * sl.tpb);
+  return blk * sl.tpb * ndig + (int64_t)dg * tin + tib;
+}
+
+// K2a: per-tile digit histogram.
 __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(
     const uint32_t* __restrict__ keys, int64_t n, int shift, int bits,
-    uint32_t* __restrict__ hist, int64_t ntiles) {
+    uint32_t* __restrict__ hist, SegLayout sl) {
   __shared__ uint32_t cnt[1 << kMaxDigitBits];
   const int ndig = 1 << bits;
   const uint32_t mask = ndig - 1;
@@ -72,7 +89,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(
   }
   __syncthreads();
   for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x)
-    hist[(int64_t)dgt * ntiles + blockIdx.x] = cnt[dgt];
+    hist[hist_index(sl, blockIdx.x, dgt, ndig)] = cnt[dgt];
 }
 
 // Exclusive scan of a uint32 array (3 phases).  Block = 256 threads x 16 items = 4096.
@@ -165,31 +182,45 @@ __global__ void __launch_bounds__(256) scan_down_kernel(const uint32_t* __restri
 // 16 rounds of 32 consecutive elements; ranks within the warp come from warp-private digit
 // counters (match_any groups equal digits in a round, lower lanes first), ranks across warps
 // from an exclusive prefix over the warp counters, ranks across tiles from the scanned
-// digit-major histogram.  Element order inside the tile is therefore preserved.
+// histogram.  Element order inside the tile is therefore preserved.  The tile is first reordered
+// by digit in shared memory and then written out in digit runs (coalesced stores).
+// vin == nullptr: values are the element indices (first pass; identity permutation).
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift, int bits,
-    const uint32_t* __restrict__ hist_scan, int64_t ntiles) {
+    const uint32_t* __restrict__ hist_scan, SegLayout sl) {
   constexpr int kWarps = kSortThreads / 32;
   constexpr int kPerWarp = kSortTile / kWarps;   // 512
   __shared__ uint32_t wcnt[kWarps][1 << kMaxDigitBits];
   __shared__ uint32_t gbase[1 << kMaxDigitBits];
+  __shared__ uint32_t tstart[1 << kMaxDigitBits];
+  __shared__ uint32_t skey[kSortTile];
+  __shared__ uint32_t sval[kSortTile];
+  __shared__ uint32_t wsum[kWarps];
   const int ndig = 1 << bits;
   const uint32_t mask = ndig - 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kWarps * ndig; i += blockDim.x) wcnt[i / ndig][i % ndig] = 0;
   for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x)
-    gbase[dgt] = hist_scan[(int64_t)dgt * ntiles + blockIdx.x];
+    gbase[dgt] = hist_scan[hist_index(sl, blockIdx.x, dgt, ndig)];
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)w * kPerWarp;
+  const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
+  const int tile_n = (int)min((int64_t)kSortTile, n - tbase);
+  const int64_t base = tbase + (int64_t)w * kPerWarp;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t k[kSortItems], v[kSortItems], r[kSortItems];
+  // all loads first (independent, in flight together), then the serial ranking rounds
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     int64_t idx = base + j * 32 + lane;
     bool valid = idx < n;
-    k[j] = valid ? kin[idx] : 0u;
-    v[j] = valid ? vin[idx] : 0u;
+    k[j] = valid ? __ldg(&kin[idx]) : 0u;
+    v[j] = valid ? (vin ? __ldg(&vin[idx]) : (uint32_t)idx) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    int64_t idx = base + j * 32 + lane;
+    bool valid = idx < n;
     uint32_t dg = valid ? ((k[j] >> shift) & mask) : 0xffffffffu;
     uint32_t peers = __match_any_sync(0xffffffffu, dg);
     uint32_t cnt = valid ? wcnt[w][dg] : 0u;
@@ -199,41 +230,65 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     __syncwarp();
   }
   __syncthreads();
-  for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x) {
-    uint32_t run = 0;
+  // per digit: exclusive prefix over warps, tile count
+  uint32_t tcount = 0;
+  const int dg0 = threadIdx.x;   // ndig <= 256 = blockDim
+  if (dg0 < ndig) {
 #pragma unroll
     for (int ww = 0; ww < kWarps; ++ww) {
-      uint32_t t = wcnt[ww][dgt];
-      wcnt[ww][dgt] = run;
-      run += t;
+      uint32_t t = wcnt[ww][dg0];
+      wcnt[ww][dg0] = tcount;
+      tcount += t;
     }
   }
+  // exclusive scan of tcount over digits (block scan)
+  uint32_t x = tcount;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  uint32_t before = 0;
+  for (int ww = 0; ww < w; ++ww) before += wsum[ww];
+  if (dg0 < ndig) tstart[dg0] = before + x - tcount;
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     int64_t idx = base + j * 32 + lane;
     if (idx < n) {
       uint32_t dg = (k[j] >> shift) & mask;
-      uint32_t pos = gbase[dg] + wcnt[w][dg] + r[j];
-      kout[pos] = k[j];
-      vout[pos] = v[j];
+      uint32_t lpos = tstart[dg] + wcnt[w][dg] + r[j];
+      skey[lpos] = k[j];
+      sval[lpos] = v[j];
     }
+  }
+  __syncthreads();
+  for (int li = threadIdx.x; li < tile_n; li += kSortThreads) {
+    uint32_t kk = skey[li];
+    uint32_t dg = (kk >> shift) & mask;
+    uint32_t pos = gbase[dg] + (uint32_t)li - tstart[dg];
+    kout[pos] = kk;
+    vout[pos] = sval[li];
   }
 }
 
-// K3: sorted node copy xs[i] = x[perm[i]] and bin offsets from the sorted keys.
+// K3: sorted node copy xs[i] = x[perm[i]] and offsets over the full sort key (user block, bin):
+// key'(i) = (i >> ub_log2) * nbins + skey[i] (sorted position i lies in user block i >> ub_log2).
 __global__ void build_kernel(const double* __restrict__ x, const uint32_t* __restrict__ perm,
                              const uint32_t* __restrict__ skeys, double* __restrict__ xs,
-                             uint32_t* __restrict__ bin_start, int64_t n, int d, int64_t nbins) {
+                             uint32_t* __restrict__ key_start, int64_t n, int d, int64_t nbins,
+                             int ub_log2, int64_t nkeys) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i < n) {
       uint32_t j = perm[i];
       for (int t = 0; t < d; ++t) xs[i * d + t] = x[(int64_t)j * d + t];
     }
-    int64_t kprev = (i == 0) ? -1 : (int64_t)skeys[i - 1];
-    int64_t kcur = (i == n) ? nbins : (int64_t)skeys[i];
-    for (int64_t b = kprev + 1; b <= kcur; ++b) bin_start[b] = (uint32_t)i;
+    int64_t kprev = (i == 0) ? -1 : (((i - 1) >> ub_log2) * nbins + (int64_t)skeys[i - 1]);
+    int64_t kcur = (i == n) ? nkeys : ((i >> ub_log2) * nbins + (int64_t)skeys[i]);
+    for (int64_t b = kprev + 1; b <= kcur; ++b) key_start[b] = (uint32_t)i;
   }
 }
 
@@ -257,7 +312,8 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
   cudaError_t e = cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), p->stream);
   if (e != cudaSuccess) return e;
   if (n > 0) {
-    keys_kernel<<<grid_for(n, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0, p->d_v0, p->d_bad);
+    keys_kernel<<<grid_for(n, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0,
+                                                         p->sort_passes ? nullptr : p->d_v0, p->d_bad);
     p->launches++;
   }
   return cudaGetLastError();
@@ -273,35 +329,45 @@ static cudaError_t exclusive_scan(bnfft_plan_s* p, const uint32_t* in, uint32_t*
 }
 
 cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
-  uint32_t *kin = p->d_k0, *vin = p->d_v0, *kout = p->d_k1, *vout = p->d_v1;
+  uint32_t *kin = p->d_k0, *vin = nullptr, *kout = p->d_k1, *vout = p->d_v1;
   if (n > 0 && p->sort_passes > 0) {
-    int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+    SegLayout sl;
+    sl.ntiles = (n + kSortTile - 1) / kSortTile;
+    sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - 12));
     int bits = p->digit_bits;
     for (int pass = 0; pass < p->sort_passes; ++pass) {
       int shift = pass * bits;
       int b = std::min(bits, p->key_bits - shift);
-      int64_t nh = ((int64_t)1 << b) * ntiles;
-      radix_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, p->stream>>>(kin, n, shift, b,
-                                                                          p->d_hist, ntiles);
+      int64_t nh = ((int64_t)1 << b) * sl.ntiles;
+      radix_hist_kernel<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(kin, n, shift, b,
+                                                                             p->d_hist, sl);
       p->launches++;
       cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
       if (e != cudaSuccess) return e;
-      radix_scatter_kernel<<<(unsigned)ntiles, kSortThreads, 0, p->stream>>>(
-          kin, vin, kout, vout, n, shift, b, p->d_hist, ntiles);
+      radix_scatter_kernel<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(
+          kin, vin, kout, vout, n, shift, b, p->d_hist, sl);
       p->launches++;
       std::swap(kin, kout);
-      std::swap(vin, vout);
+      if (!vin) {
+        vin = vout;
+        vout = p->d_v0;
+      } else {
+        std::swap(vin, vout);
+      }
     }
+    p->d_skeys = kin;
+    p->d_perm = vin;
+  } else {
+    p->d_skeys = p->d_k0;
+    p->d_perm = p->d_v0;   // identity written by keys_kernel
   }
-  p->d_skeys = kin;
-  p->d_perm = vin;
   return cudaGetLastError();
 }
 
 cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n) {
   build_kernel<<<grid_for(n + 1, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys, p->d_xs,
                                                             p->d_bin_start, n, p->opts.d,
-                                                            p->nbins);
+                                                            p->nbins, p->ub_log2, p->nkeys);
   p->launches++;
   return cudaGetLastError();
 }

@@ -106,7 +106,8 @@ def test_reduced_configs(bn, torch, case):
 
 
 # ----------------------------------------------------------------------------- bin sort
-@pytest.mark.parametrize("cid,d,M,N", [(2, 1, 1 << 16, 100_000), (3, 2, 256, 70_000),
+@pytest.mark.parametrize("cid,d,M,N", [(2, 1, 1 << 16, 100_000), (2, 1, 1 << 16, 3_000_017),
+                                       (3, 2, 256, 70_000), (3, 2, 1024, 2_500_000),
                                        (4, 3, 64, 50_000), (5, 3, 64, 40_000)])
 def test_bin_sort_bit_exact(bn, torch, cid, d, M, N):
     cfg = synth.CONFIGS[cid].scaled(d=d, M=M, N=N, batch=1)
@@ -121,12 +122,47 @@ def test_bin_sort_bit_exact(bn, torch, cid, d, M, N):
     key = np.zeros(N, dtype=np.int64)
     for t in range(d):
         key = key * info.bins_per_dim[t] + (cells[:, t] >> info.bin_log2[t])
-    perm_ref, off_ref = O.stable_bin_sort(key, info.nbins)
+    # sort key (user block, bin) as documented in include/bnfft.h (bnfft_info)
+    key = (np.arange(N, dtype=np.int64) >> info.user_block_log2) * info.nbins + key
+    assert info.nkeys == (((N - 1) >> info.user_block_log2) + 1) * info.nbins
+    perm_ref, off_ref = O.stable_bin_sort(key, int(info.nkeys))
     perm = plan.perm().cpu().numpy().astype(np.int64)
     off = plan.bin_offsets().cpu().numpy().astype(np.int64)
     assert np.array_equal(perm, perm_ref)
     assert np.array_equal(off, off_ref)
     plan.close()
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("window", ["sinh", "gauss", "ckb"])
+def test_exact_taps_path(bn, torch, prec, window):
+    """BNFFT_EXACT_TAPS (direct sinc * phi) and the default tap polynomials both meet parity."""
+    cfg = synth.CONFIGS[2].scaled(M=1 << 10, m=6, N=20_011)
+    x = synth.make_nodes(cfg, variant=6)
+    fh = synth.make_spectrum(cfg, variant=6, prec=prec)
+    ref = oracle_f(x, fh, cfg.M, 2.0, 6, window)["f"]
+    for exact in (False, True):
+        f, plan = run_gpu(bn, torch, x, fh, 1, cfg.M, 2.0, 6, window, prec, exact_taps=exact)
+        assert plan.info().tap_poly == (0 if exact else 1)
+        assert rel_l2(f, ref) <= TOL[prec]
+        plan.close()
+
+
+def test_tap_fit_check_consistent_for_sharp_shapes(bn, torch):
+    """Very sharp sinh windows: whatever the plan-time fit check decides (tap polynomials or the
+    exact fallback), the decision matches the reported fit error and parity holds."""
+    M, m = 256, 6
+    x = synth.make_nodes(synth.CONFIGS[1], N=5000)
+    rng = np.random.default_rng(3)
+    fh = rng.standard_normal((1, M)) + 1j * rng.standard_normal((1, M))
+    for prec, beta in (("c128", 150.0), ("c128", 60.0), ("c64", 60.0)):
+        f, plan = run_gpu(bn, torch, x, fh, 1, M, 2.0, m, "sinh", prec, shape=beta)
+        info = plan.info()
+        tol = 1e-13 if prec == "c128" else 2e-6
+        assert info.tap_poly == (1 if info.tap_fit_err <= tol else 0)
+        ref = O.algorithm2(x, fh, M, 2.0, m, "sinh", shape=beta)["f"]
+        assert rel_l2(f, ref) <= TOL[prec]
+        plan.close()
 
 
 # ----------------------------------------------------------------------------- exactness / determinism
