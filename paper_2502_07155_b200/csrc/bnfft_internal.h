@@ -121,6 +121,7 @@ struct bnfft_plan_s {
   int gather_bt = 1;          // batch slice per staged box
   int gather_smax = 1;        // segments (bins) staged per round
   int gather_box_cap = 0;     // d = 1: staged window capacity (complex elements)
+  int64_t gather_grid1 = 0;   // d = 1: persistent grid size (SMs x resident CTAs)
   size_t gather_smem = 0;
 
   // timing

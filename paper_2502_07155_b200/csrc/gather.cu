@@ -5,7 +5,8 @@
 
 namespace bnfft {
 
-static const void* select_kernel(int d, int m, bool c128, bool poly) {
+static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false) {
+  if (d == 1 && batched) return c128 ? gather_kernel_1d(m + 100, poly) : gather_kernel_1f(m + 100, poly);
   if (d == 1) return c128 ? gather_kernel_1d(m, poly) : gather_kernel_1f(m, poly);
   if (d == 2) return c128 ? gather_kernel_2d(m, poly) : gather_kernel_2f(m, poly);
   if (d == 3) return c128 ? gather_kernel_3d(m, poly) : gather_kernel_3f(m, poly);
@@ -32,15 +33,23 @@ static size_t smem_budget() { return 40u << 10; }
 constexpr int kMaxSegPerRound = 32;
 
 cudaError_t gather_prepare(bnfft_plan_s* p) {
-  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly);
+  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1);
   if (!fn) return cudaErrorInvalidValue;
-  if (p->opts.d == 1) {
-    // one contiguous window per CTA chunk; capacity 32 KB
-    p->gather_box_cap = (int)((32u << 10) / p->csize);
-    p->gather_smem = (size_t)p->gather_box_cap * p->csize;
+  if (p->opts.d == 1 && p->opts.batch == 1) {
+    // two contiguous windows (double buffer) of 12 KB each; persistent grid sized by occupancy
+    p->gather_box_cap = (int)((12u << 10) / p->csize);
+    p->gather_smem = 2 * (size_t)p->gather_box_cap * p->csize;
     p->gather_bt = 1;
     p->gather_smax = 1;
-    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, nsm = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGatherThreads, p->gather_smem);
+    if (e != cudaSuccess) return e;
+    p->gather_grid1 = (int64_t)std::max(1, per_sm) * nsm;
+    return cudaSuccess;
   }
   size_t per = gather_box_elems(p) * p->csize;
   int bt = (int)std::max<size_t>(1, std::min<size_t>((size_t)p->opts.batch, smem_budget() / per));
@@ -81,14 +90,23 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
   gp.wp = p->wp;
   gp.boxcap = p->gather_box_cap;
   constexpr int NC = PolyN<R>::NC;
+  constexpr int NH = PolyH<R>::NH;
+  static_assert(2 * NH == NC, "even/odd split of the tap polynomials");
   if (p->tap_poly) {
-    const int T = 2 * p->opts.m;
-    for (int i = 0; i < T; ++i)
-      for (int k = 0; k < NC; ++k) gp.coef[k][i] = (R)p->tap_coef[(size_t)i * NC + k];
+    for (int i = 0; i < p->opts.m; ++i)      // taps i < m; the others by mirror symmetry
+      for (int k = 0; k < NH; ++k) {
+        gp.ceo[k][i][0] = (R)p->tap_coef[(size_t)i * NC + 2 * k];
+        gp.ceo[k][i][1] = (R)p->tap_coef[(size_t)i * NC + 2 * k + 1];
+      }
   }
   void* args[] = {&gp};
-  const int64_t per_cta = p->opts.d == 1 ? (int64_t)kGatherThreads * kNPT1 : kGatherThreads;
-  unsigned blocks = (unsigned)((p->n + per_cta - 1) / per_cta);
+  unsigned blocks;
+  if (p->opts.d == 1 && p->opts.batch == 1) {
+    const int64_t ch = (int64_t)kGatherThreads * NPT1<R>::v;
+    blocks = (unsigned)std::min<int64_t>((p->n + ch - 1) / ch, p->gather_grid1);
+  } else {
+    blocks = (unsigned)((p->n + kGatherThreads - 1) / kGatherThreads);
+  }
   cudaError_t e = cudaLaunchKernel(fn, dim3(blocks), dim3(kGatherThreads), args, p->gather_smem,
                                    p->stream);
   p->launches++;
@@ -97,7 +115,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
 
 cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
   if (p->n == 0) return cudaSuccess;
-  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly);
+  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1);
   if (!fn) return cudaErrorInvalidValue;
   return p->c128 ? launch_gather_t<double>(p, out, fn) : launch_gather_t<float>(p, out, fn);
 }

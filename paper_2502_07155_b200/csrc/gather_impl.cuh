@@ -37,6 +37,10 @@ template <> struct CT<double> { using C = double2; };
 template <typename R> struct PolyN;
 template <> struct PolyN<float> { static constexpr int NC = 10; };   // degree 9
 template <> struct PolyN<double> { static constexpr int NC = 18; };  // degree 17
+// Mirror symmetry: psi is even, so w_{2m-1-i}(u) = w_i(1-u), i.e. P_{2m-1-i}(x) = P_i(-x).  Only
+// taps i < m are stored, split into even/odd parts P_i(x) = E_i(x^2) + x O_i(x^2); one Horner pass
+// in y = x^2 over the pair (E_i, O_i) then gives both w_i = E + xO and w_{2m-1-i} = E - xO.
+template <typename R> struct PolyH { static constexpr int NH = PolyN<R>::NC / 2; };
 
 constexpr int kMaxTaps = 32;
 
@@ -57,7 +61,7 @@ struct GatherParams {
   R inv_m;
   int boxcap;             // d = 1 kernel: staged-box capacity in complex elements
   WinParams wp;
-  alignas(16) R coef[PolyN<R>::NC][kMaxTaps];   // degree-major: coef[k][i] of tap i
+  alignas(16) R ceo[PolyH<R>::NH][kMaxTaps / 2][2];   // [k][i][0] = E_i coeff k, [k][i][1] = O_i
 };
 
 __device__ __forceinline__ double sinpi_r(double u) { return sinpi(u); }
@@ -106,12 +110,19 @@ __device__ __forceinline__ DimState<R> dim_state(double u_d, const GatherParams<
 template <int T, typename R, bool POLY>
 __device__ __forceinline__ R tap_weight(const DimState<R>& st, int i, const GatherParams<R>& p) {
   constexpr int m = T / 2;
-  constexpr int NC = PolyN<R>::NC;
   if (st.hit >= 0) return i == st.hit ? R(1) : R(0);
   if (POLY) {
-    R h = p.coef[NC - 1][i];
+    constexpr int NH = PolyH<R>::NH;
+    const int ii = i < m ? i : T - 1 - i;
+    const R xs = i < m ? st.x : -st.x;
+    const R y = st.x * st.x;
+    R e = p.ceo[NH - 1][ii][0], o = p.ceo[NH - 1][ii][1];
 #pragma unroll
-    for (int k = NC - 2; k >= 0; --k) h = fma(h, st.x, p.coef[k][i]);
+    for (int k = NH - 2; k >= 0; --k) {
+      e = fma(e, y, p.ceo[k][ii][0]);
+      o = fma(o, y, p.ceo[k][ii][1]);
+    }
+    R h = fma(xs, o, e);
     if (i == 0) h *= st.sq0;
     if (i == T - 1) h *= st.sq1;
     return h;
@@ -123,8 +134,9 @@ __device__ __forceinline__ R tap_weight(const DimState<R>& st, int i, const Gath
   }
 }
 
-// All T taps of one dimension.  POLY: Horner in x = 2u-1; the float path evaluates tap pairs with
-// packed FFMA2 (sm_100 fma.rn.f32x2), the coefficient pair coming from the kernel parameters.
+// All T taps of one dimension.  POLY: one Horner pass in y = x^2 over the (E_i, O_i) pairs of the
+// m stored taps, packed FFMA2 (sm_100 fma.rn.f32x2) for float with the coefficient pair taken from
+// the kernel parameters; then w_i = E + xO and w_{2m-1-i} = E - xO.
 template <int T, bool POLY>
 __device__ __forceinline__ void all_taps(const DimState<float>& st, const GatherParams<float>& p,
                                          float (&w)[T]) {
@@ -133,15 +145,19 @@ __device__ __forceinline__ void all_taps(const DimState<float>& st, const Gather
     for (int k = 0; k < T; ++k) w[k] = tap_weight<T, float, POLY>(st, k, p);
     return;
   }
-  constexpr int NC = PolyN<float>::NC;
-  const float2 xx = make_float2(st.x, st.x);
+  constexpr int NH = PolyH<float>::NH;
+  constexpr int m = T / 2;
+  const float y = st.x * st.x;
+  const float2 yy = make_float2(y, y);
+  const float2 xm = make_float2(st.x, -st.x);
 #pragma unroll
-  for (int j = 0; j < T / 2; ++j) {
-    float2 h = reinterpret_cast<const float2*>(p.coef[NC - 1])[j];
+  for (int i = 0; i < m; ++i) {
+    float2 h = *reinterpret_cast<const float2*>(p.ceo[NH - 1][i]);
 #pragma unroll
-    for (int k = NC - 2; k >= 0; --k) h = __ffma2_rn(h, xx, reinterpret_cast<const float2*>(p.coef[k])[j]);
-    w[2 * j] = h.x;
-    w[2 * j + 1] = h.y;
+    for (int k = NH - 2; k >= 0; --k) h = __ffma2_rn(h, yy, *reinterpret_cast<const float2*>(p.ceo[k][i]));
+    const float2 r = __ffma2_rn(xm, make_float2(h.y, h.y), make_float2(h.x, h.x));
+    w[i] = r.x;
+    w[T - 1 - i] = r.y;
   }
   w[0] *= st.sq0;
   w[T - 1] *= st.sq1;
@@ -150,8 +166,27 @@ __device__ __forceinline__ void all_taps(const DimState<float>& st, const Gather
 template <int T, bool POLY>
 __device__ __forceinline__ void all_taps(const DimState<double>& st, const GatherParams<double>& p,
                                          double (&w)[T]) {
+  if (!POLY || st.hit >= 0) {
 #pragma unroll
-  for (int k = 0; k < T; ++k) w[k] = tap_weight<T, double, POLY>(st, k, p);
+    for (int k = 0; k < T; ++k) w[k] = tap_weight<T, double, POLY>(st, k, p);
+    return;
+  }
+  constexpr int NH = PolyH<double>::NH;
+  constexpr int m = T / 2;
+  const double y = st.x * st.x;
+#pragma unroll
+  for (int i = 0; i < m; ++i) {
+    double e = p.ceo[NH - 1][i][0], o = p.ceo[NH - 1][i][1];
+#pragma unroll
+    for (int k = NH - 2; k >= 0; --k) {
+      e = fma(e, y, p.ceo[k][i][0]);
+      o = fma(o, y, p.ceo[k][i][1]);
+    }
+    w[i] = fma(st.x, o, e);
+    w[T - 1 - i] = fma(-st.x, o, e);
+  }
+  w[0] *= st.sq0;
+  w[T - 1] *= st.sq1;
 }
 
 // acc += w * g  (complex g, real w)
@@ -323,112 +358,227 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const __grid_con
   }
 }
 
-// d = 1 gather.  CTA k owns sorted nodes [k*256*NPT, (k+1)*256*NPT) (thread t takes
-// k*256*NPT + j*256 + t, j < NPT: coalesced loads).  The nodes are sorted by bin inside user
-// blocks, so the chunk's cells span a short range [cmin, cmax]: the grid window
-// [cmin-m+1, cmax+m] (zero outside I_L) is staged once into shared memory with contiguous loads.
-// If the window exceeds the box capacity (sparse node sets) the taps are read straight from
-// global memory through L1 instead.
-constexpr int kNPT1 = 4;
+// d = 1 gather: persistent CTAs, TMA bulk-copy staging, software pipeline.
+//
+// Chunk k = sorted nodes [k*CH, (k+1)*CH), CH = 256*NPT (thread t takes k*CH + j*256 + t).  Nodes
+// are sorted by bin inside user blocks, so a chunk's cells span a short range [cmin, cmax]; its grid
+// window [cmin-m+1, cmax+m] is one contiguous range of theta, staged into shared memory by a single
+// cp.async.bulk (TMA, completion on an mbarrier); parts outside I_L are zero-filled (reading A5).
+// Per CTA iteration (chunk k): the window of chunk k+G is issued (its node data arrived during the
+// previous iteration), the node data of chunk k+2G is loaded into registers, then chunk k is
+// computed from its window, so both the node loads and the window copy overlap compute.  Windows
+// larger than the buffer (sparse node sets) fall back to direct global loads for that chunk.
+template <typename R> struct NPT1 { static constexpr int v = sizeof(R) == 4 ? 4 : 2; };
 
-template <int T, typename R, bool POLY>
-__global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_constant__ GatherParams<R> p) {
-  using C = typename CT<R>::C;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* box = reinterpret_cast<C*>(smem_raw);
-  __shared__ int s_min[kGatherThreads / 32], s_max[kGatherThreads / 32];
-  constexpr int m = T / 2;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t base = (int64_t)blockIdx.x * kGatherThreads * kNPT1;
-  int cell[kNPT1];
-  double uu[kNPT1];
-  uint32_t dst[kNPT1];
-  int cmin = 0x7fffffff, cmax = -1;
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <typename R, int NPT>
+struct NodeSet1 {
+  double x[NPT];
+  uint32_t dst[NPT];
+};
+
+template <typename R, int NPT>
+__device__ __forceinline__ void load_nodes1(const GatherParams<R>& p, int64_t chunk, NodeSet1<R, NPT>& ns) {
+  const int64_t base = chunk * (int64_t)kGatherThreads * NPT + threadIdx.x;
 #pragma unroll
-  for (int j = 0; j < kNPT1; ++j) {
-    const int64_t i = base + j * kGatherThreads + tid;
-    cell[j] = -1;
+  for (int j = 0; j < NPT; ++j) {
+    const int64_t i = base + j * kGatherThreads;
     if (i < p.n) {
-      dst[j] = __ldg(&p.perm[i]);
-      const double Lx = __dmul_rn(p.Lf, __ldg(&p.xs[i]));
-      const double fl = floor(Lx);
-      double u = Lx - fl;
-      int64_t c = (int64_t)fl + p.L / 2;
-      if (c > p.L - 1) { c = p.L - 1; u = 1.0; }
-      cell[j] = (int)c;
-      uu[j] = u;
-      cmin = min(cmin, (int)c);
-      cmax = max(cmax, (int)c);
-    }
-  }
-  cmin = __reduce_min_sync(0xffffffffu, cmin);
-  cmax = __reduce_max_sync(0xffffffffu, cmax);
-  if (lane == 0) {
-    s_min[wid] = cmin;
-    s_max[wid] = cmax;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int w2 = 0; w2 < kGatherThreads / 32; ++w2) {
-    cmin = min(cmin, s_min[w2]);
-    cmax = max(cmax, s_max[w2]);
-  }
-  const int64_t lo = (int64_t)cmin - (m - 1);
-  const int nbox = cmax - cmin + T;
-  const C* __restrict__ grid = (const C*)p.grid;
-  C* __restrict__ out = (C*)p.out;
-  const int nbt_cap = p.boxcap / nbox;            // spectra per staged slice (0: not staged)
-  const int step = nbt_cap > 0 ? min(nbt_cap, p.batch) : p.batch;
-  for (int b0 = 0; b0 < p.batch; b0 += step) {
-    const int nbt = min(step, p.batch - b0);
-    if (nbt_cap > 0) {
-      if (b0 > 0) __syncthreads();
-      for (int bb = 0; bb < nbt; ++bb) {
-        const C* src = grid + (int64_t)(b0 + bb) * p.Ld;
-        for (int q = tid; q < nbox; q += kGatherThreads) {
-          const int64_t pos = lo + q;
-          box[bb * nbox + q] = (pos >= 0 && pos < p.L) ? __ldg(&src[pos]) : czero<C>();
-        }
-      }
-      __syncthreads();
-    }
-#pragma unroll 1
-    for (int j = 0; j < kNPT1; ++j) {
-      if (cell[j] < 0) continue;
-      const DimState<R> st = dim_state<T, R, POLY>(uu[j], p);
-      R w[T];
-      all_taps<T, POLY>(st, p, w);
-      for (int bb = 0; bb < nbt; ++bb) {
-        C acc = czero<C>();
-        if (nbt_cap > 0) {
-          const C* row = box + bb * nbox + (cell[j] - cmin);
-#pragma unroll
-          for (int k = 0; k < T; ++k) cmac(acc, w[k], row[k]);
-        } else {
-          const C* src = grid + (int64_t)(b0 + bb) * p.Ld;
-          const int64_t l0 = (int64_t)cell[j] - (m - 1);
-          if (l0 >= 0 && l0 + T <= p.L) {
-#pragma unroll
-            for (int k = 0; k < T; ++k) cmac(acc, w[k], __ldg(&src[l0 + k]));
-          } else {
-#pragma unroll
-            for (int k = 0; k < T; ++k) {
-              const int64_t pos = l0 + k;
-              if (pos >= 0 && pos < p.L) cmac(acc, w[k], __ldg(&src[pos]));
-            }
-          }
-        }
-        out[(int64_t)(b0 + bb) * p.n + dst[j]] = acc;
-      }
+      ns.x[j] = __ldg(&p.xs[i]);
+      ns.dst[j] = __ldg(&p.perm[i]);
+    } else {
+      ns.x[j] = 2.0;   // marks an inactive slot (valid nodes lie in [-1/2, 1/2))
+      ns.dst[j] = 0;
     }
   }
 }
 
+// cell c in [0, L) and u in [0, 1]; returns false for inactive slots.
+__device__ __forceinline__ bool node_cell(double xv, double Lf, int64_t L, int& c, double& u) {
+  if (xv > 1.0) return false;
+  const double Lx = __dmul_rn(Lf, xv);
+  const double fl = floor(Lx);
+  u = Lx - fl;
+  int64_t cc = (int64_t)fl + L / 2;
+  if (cc > L - 1) { cc = L - 1; u = 1.0; }   // fl(L x) == L/2 (defensive)
+  c = (int)cc;
+  return true;
+}
+
+struct Window1 {
+  int64_t lo;      // grid index of buffer element 0 (16-byte aligned)
+  int nbox;        // elements in the window
+  int staged;      // 1: in shared memory, 0: read from global
+};
+
+// Block-wide cell range of a chunk -> window; thread 0 issues the bulk copy, all threads zero-fill
+// the parts outside [0, L).  Contains one __syncthreads.
+template <int T, typename R, int NPT>
+__device__ __forceinline__ Window1 issue_window1(const GatherParams<R>& p, const NodeSet1<R, NPT>& ns,
+                                                 typename CT<R>::C* buf, uint64_t* bar, int* s_red) {
+  using C = typename CT<R>::C;
+  constexpr int m = T / 2;
+  constexpr int kAl = 16 / sizeof(C);   // elements per 16 bytes
+  int cmin = 0x7fffffff, cmax = -1;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    int c;
+    double u;
+    if (node_cell(ns.x[j], p.Lf, p.L, c, u)) {
+      cmin = min(cmin, c);
+      cmax = max(cmax, c);
+    }
+  }
+  cmin = __reduce_min_sync(0xffffffffu, cmin);
+  cmax = __reduce_max_sync(0xffffffffu, cmax);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_red[wid] = cmin;
+    s_red[8 + wid] = cmax;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int w2 = 0; w2 < kGatherThreads / 32; ++w2) {
+    cmin = min(cmin, s_red[w2]);
+    cmax = max(cmax, s_red[8 + w2]);
+  }
+  Window1 win;
+  int64_t lo = (int64_t)cmin - (m - 1);
+  lo -= ((lo % kAl) + kAl) % kAl;                       // align down (lo may be negative)
+  int64_t hi = (int64_t)cmax + m + 1;                   // exclusive
+  hi += (kAl - (hi - lo) % kAl) % kAl;
+  win.lo = lo;
+  win.nbox = (int)(hi - lo);
+  win.staged = win.nbox <= p.boxcap;
+  if (win.staged) {
+    const int64_t g0 = lo > 0 ? lo : (int64_t)0, g1 = hi < p.L ? hi : p.L;
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)((g1 - g0) * (int64_t)sizeof(C));
+      mbar_expect_tx(bar, bytes);
+      if (bytes) tma_bulk_g2s(buf + (g0 - lo), (const C*)p.grid + g0, bytes, bar);
+    }
+    // zero extension outside I_L (generic stores, disjoint from the TMA range)
+    for (int64_t q = threadIdx.x; q < g0 - lo; q += kGatherThreads) buf[q] = czero<C>();
+    for (int64_t q = (g1 - lo) + threadIdx.x; q < hi - lo; q += kGatherThreads) buf[q] = czero<C>();
+  }
+  return win;
+}
+
+template <int T, typename R, bool POLY>
+__global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_constant__ GatherParams<R> p) {
+  using C = typename CT<R>::C;
+  constexpr int NPT = NPT1<R>::v;
+  constexpr int m = T / 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  C* buf0 = reinterpret_cast<C*>(smem_raw);
+  C* buf1 = buf0 + p.boxcap;
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ int s_red[16];
+  const int64_t CH = (int64_t)kGatherThreads * NPT;
+  const int64_t nchunks = (p.n + CH - 1) / CH;
+  const int64_t G = gridDim.x;
+  int64_t k = blockIdx.x;
+  if (k >= nchunks) return;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const C* __restrict__ grid = (const C*)p.grid;
+  C* __restrict__ out = (C*)p.out;
+
+  NodeSet1<R, NPT> cur, nxt;
+  load_nodes1<R, NPT>(p, k, cur);
+  Window1 wcur = issue_window1<T, R, NPT>(p, cur, buf0, &bars[0], s_red);
+  if (k + G < nchunks) load_nodes1<R, NPT>(p, k + G, nxt);
+  uint32_t phases = 0u;   // bit b: parity of the next completion of bars[b]
+  for (int it = 0; k < nchunks; ++it, k += G) {
+    const int b = it & 1;
+    C* bcur = b ? buf1 : buf0;
+    // (1) window of chunk k+G into the other buffer (its previous user, chunk k-G, finished before
+    //     the barrier inside issue_window1)
+    Window1 wnxt{0, 0, 0};
+    if (k + G < nchunks) wnxt = issue_window1<T, R, NPT>(p, nxt, b ? buf0 : buf1, &bars[b ^ 1], s_red);
+    else __syncthreads();   // zero-fill of the current window visible to all threads
+    // (2) node data of chunk k+2G into registers (in flight during the compute below)
+    NodeSet1<R, NPT> nn;
+    if (k + 2 * G < nchunks) load_nodes1<R, NPT>(p, k + 2 * G, nn);
+    // (3) compute chunk k
+    if (wcur.staged) {
+      mbar_wait(&bars[b], (phases >> b) & 1u);
+      phases ^= 1u << b;
+    }
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      int c;
+      double u;
+      if (!node_cell(cur.x[j], p.Lf, p.L, c, u)) continue;
+      const DimState<R> st = dim_state<T, R, POLY>(u, p);
+      R w[T];
+      all_taps<T, POLY>(st, p, w);
+      C acc = czero<C>();
+      if (wcur.staged) {
+        const C* row = bcur + (c - (m - 1) - wcur.lo);
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) cmac(acc, w[kk], row[kk]);
+      } else {
+        const int64_t l0 = (int64_t)c - (m - 1);
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) {
+          const int64_t pos = l0 + kk;
+          if (pos >= 0 && pos < p.L) cmac(acc, w[kk], __ldg(&grid[pos]));
+        }
+      }
+      out[cur.dst[j]] = acc;
+    }
+    cur = nxt;
+    nxt = nn;
+    wcur = wnxt;
+  }
+}
+
+// D == 1: the pipelined window kernel (batch == 1) or, for batched d = 1 plans, the generic
+// segment kernel (returned for m + 100).
 template <int D, typename R, bool POLY, int MM>
 static const void* kernel_for(int m) {
   if (m == MM) {
     if constexpr (D == 1) return (const void*)gather1_kernel<2 * MM, R, POLY>;
     else return (const void*)gather_kernel<D, 2 * MM, R, POLY>;
+  }
+  if constexpr (D == 1) {
+    if (m == MM + 100) return (const void*)gather_kernel<1, 2 * MM, R, POLY>;
   }
   if constexpr (MM > 1) return kernel_for<D, R, POLY, MM - 1>(m);
   return nullptr;

@@ -186,19 +186,32 @@ __global__ void tapcheck_kernel(int T, int NC, WinParams wp, int edge_sqrt, int 
     const double u = j / 1024.0;
     if (u == 0.0 || u == 1.0) continue;   // Kronecker branch in the gather
     const double ex = tap_exact_d(i, u, m, wp, edge_sqrt, false);
+    // the gather stores taps i < m only and evaluates tap 2m-1-i as P_i(-x) (mirror symmetry)
+    const int ii = i < m ? i : T - 1 - i;
+    const double sgn = i < m ? 1.0 : -1.0;
     double ap;
     if (fp32) {
-      const float x = (float)(2.0 * u - 1.0);
-      float h = (float)coef[i * NC + NC - 1];
-      for (int k = NC - 2; k >= 0; --k) h = fmaf(h, x, (float)coef[i * NC + k]);
+      const float xf = (float)(2.0 * u - 1.0);
+      const float yf = xf * xf;
+      float e = (float)coef[ii * NC + NC - 2], o = (float)coef[ii * NC + NC - 1];
+      for (int k = NC / 2 - 2; k >= 0; --k) {
+        e = fmaf(e, yf, (float)coef[ii * NC + 2 * k]);
+        o = fmaf(o, yf, (float)coef[ii * NC + 2 * k + 1]);
+      }
+      float h = fmaf((float)sgn * xf, o, e);
       float uf = (float)u;
       if (edge_sqrt && i == 0) h *= sqrtf((1.0f - uf) * (float(2 * m - 1) + uf)) * (1.0f / m);
       if (edge_sqrt && i == T - 1) h *= sqrtf(uf * (float(2 * m) - uf)) * (1.0f / m);
       ap = h;
     } else {
       const double x = 2.0 * u - 1.0;
-      double h = coef[i * NC + NC - 1];
-      for (int k = NC - 2; k >= 0; --k) h = fma(h, x, coef[i * NC + k]);
+      const double y = x * x;
+      double e = coef[ii * NC + NC - 2], o = coef[ii * NC + NC - 1];
+      for (int k = NC / 2 - 2; k >= 0; --k) {
+        e = fma(e, y, coef[ii * NC + 2 * k]);
+        o = fma(o, y, coef[ii * NC + 2 * k + 1]);
+      }
+      double h = fma(sgn * x, o, e);
       if (edge_sqrt && i == 0) h *= sqrt((1.0 - u) * (double(2 * m - 1) + u)) / m;
       if (edge_sqrt && i == T - 1) h *= sqrt(u * (double(2 * m) - u)) / m;
       ap = h;

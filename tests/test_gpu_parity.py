@@ -87,6 +87,9 @@ CASES = [
     ("d2-gauss-c128", 3, 2, 64, 7, 7_777, 2, "gauss", "c128"),
     ("d1-m1-c128", 1, 1, 64, 1, 3_001, 1, "sinh", "c128"),
     ("d1-m16-c64", 2, 1, 512, 16, 12_345, 1, "sinh", "c64"),
+    ("d1-batch3-c128", 2, 1, 1 << 10, 8, 20_000, 3, "sinh", "c128"),
+    ("d1-batch4-c64", 2, 1, 1 << 10, 6, 20_000, 4, "gauss", "c64"),
+    ("d1-sparse-c64", 2, 1, 1 << 16, 8, 3_000, 1, "sinh", "c64"),
 ]
 
 
