@@ -172,11 +172,12 @@ BNFFT_API int bnfft_reset_timing(struct bnfft_plan_s* plan);
  *                     l_t + L/2, row-major) into a device buffer of grid_bytes.
  *   bnfft_get_perm:   n uint32: sorted position -> user index, into a device buffer.
  *   bnfft_get_bin_offsets: nkeys+1 uint32: first sorted position of each sort key (user block,
- *                     bin), into a device buffer. */
+ *                     bin), into a device buffer (built on demand for plans that keep the nodes
+ *                     in user order; see user_block_log2). */
 BNFFT_API int bnfft_get_psihat(const struct bnfft_plan_s* plan, double* host_out);
 BNFFT_API int bnfft_get_grid(const struct bnfft_plan_s* plan, void* dev_out);
 BNFFT_API int bnfft_get_perm(const struct bnfft_plan_s* plan, uint32_t* dev_out);
-BNFFT_API int bnfft_get_bin_offsets(const struct bnfft_plan_s* plan, uint32_t* dev_out);
+BNFFT_API int bnfft_get_bin_offsets(struct bnfft_plan_s* plan, uint32_t* dev_out);
 
 /* Release every resource of the plan (after synchronizing its stream).  NULL is a no-op. */
 BNFFT_API int bnfft_destroy(struct bnfft_plan_s* plan);

@@ -13,8 +13,8 @@
 namespace bnfft {
 
 constexpr int kGatherThreads = 256;   // nodes per gather CTA chunk (one node per thread)
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;        // keys per thread per tile
+constexpr int kSortThreads = 512;
+constexpr int kSortItems = 8;         // keys per thread per tile
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kMaxDigitBits = 8;
 constexpr int kQuadN = 64;            // Gauss-Legendre points for psi^ (reading A4)
@@ -102,7 +102,9 @@ struct bnfft_plan_s {
   // nodes
   int64_t n = 0, cap = 0;
   bool nodes_set = false;
-  double* d_xs = nullptr;        // sorted nodes n x d
+  double* d_xs = nullptr;        // nodes n x d: sorted (xs_user false) or user order (xs_user true)
+  bool xs_user = false;          // d <= 2 user-blocked plans keep nodes in user order
+  bool offsets_valid = false;    // key offsets built (lazily for xs_user plans)
   uint32_t* d_perm = nullptr;    // sorted pos -> user index
   uint32_t* d_skeys = nullptr;   // sorted keys (points into keys buffers)
   uint32_t* d_bin_start = nullptr;  // nkeys + 1: first sorted position of each (user block, bin)
@@ -147,6 +149,7 @@ cudaError_t launch_psihat(bnfft_plan_s* p);
 cudaError_t launch_tapfit(bnfft_plan_s* p, int NC, double* d_coef, double* d_err);
 cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n);
 cudaError_t launch_sort(bnfft_plan_s* p, int64_t n);
+cudaError_t sort_prepare();
 cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n);
 cudaError_t launch_deconv(bnfft_plan_s* p, const void* fhat);
 cudaError_t launch_gather(bnfft_plan_s* p, void* out);

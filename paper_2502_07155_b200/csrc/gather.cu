@@ -89,6 +89,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
   gp.inv_m = (R)(1.0 / p->opts.m);
   gp.wp = p->wp;
   gp.boxcap = p->gather_box_cap;
+  gp.xs_user = p->xs_user ? 1 : 0;
   constexpr int NC = PolyN<R>::NC;
   constexpr int NH = PolyH<R>::NH;
   static_assert(2 * NH == NC, "even/odd split of the tap polynomials");

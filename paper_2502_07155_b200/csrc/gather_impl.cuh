@@ -60,6 +60,7 @@ struct GatherParams {
   int edge_sqrt;          // sinh window: edge taps carry sqrt(1-(tau/m)^2)
   R inv_m;
   int boxcap;             // d = 1 kernel: staged-box capacity in complex elements
+  int xs_user;            // xs in user order: node i of the sorted order is xs[perm[i]]
   WinParams wp;
   alignas(16) R ceo[PolyH<R>::NH][kMaxTaps / 2][2];   // [k][i][0] = E_i coeff k, [k][i][1] = O_i
 };
@@ -225,9 +226,10 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const __grid_con
   uint32_t key = 0xffffffffu, dst = 0;
   if (active) {
     dst = p.perm[i];
+    const int64_t src = p.xs_user ? (int64_t)dst : i;
 #pragma unroll
     for (int t = 0; t < D; ++t) {
-      double xv = p.xs[i * D + t];
+      double xv = p.xs[src * D + t];
       double Lx = __dmul_rn(p.Lf, xv);
       double fl = floor(Lx);
       double u = Lx - fl;
@@ -415,8 +417,8 @@ __device__ __forceinline__ void load_nodes1(const GatherParams<R>& p, int64_t ch
   for (int j = 0; j < NPT; ++j) {
     const int64_t i = base + j * kGatherThreads;
     if (i < p.n) {
-      ns.x[j] = __ldg(&p.xs[i]);
       ns.dst[j] = __ldg(&p.perm[i]);
+      ns.x[j] = __ldg(&p.xs[p.xs_user ? (int64_t)ns.dst[j] : i]);
     } else {
       ns.x[j] = 2.0;   // marks an inactive slot (valid nodes lie in [-1/2, 1/2))
       ns.dst[j] = 0;

@@ -304,6 +304,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     } else {
       p->ub_log2 = 31;
     }
+    p->xs_user = p->ub_log2 < 31;
   }
 
   int rc = BNFFT_OK;
@@ -359,6 +360,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
                     !(o->flags & BNFFT_EXACT_TAPS);
     }
     CK(gather_prepare(p), "gather kernel attributes");
+    CK(sort_prepare(), "sort kernel attributes");
 
     int n[3] = {(int)L, (int)L, (int)L};
     size_t ws = 0;
@@ -455,9 +457,13 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
   timer_begin(p, ST_SORT, &ev);
   if ((e = launch_sort(p, n)) != cudaSuccess) return cuda_fail(e, "sort kernels");
   timer_end(p, ST_SORT, ev);
-  timer_begin(p, ST_BUILD, &ev);
-  if ((e = launch_build(p, x, n)) != cudaSuccess) return cuda_fail(e, "build kernel");
-  timer_end(p, ST_BUILD, ev);
+  p->offsets_valid = false;
+  if (!p->xs_user) {
+    timer_begin(p, ST_BUILD, &ev);
+    if ((e = launch_build(p, x, n)) != cudaSuccess) return cuda_fail(e, "build kernel");
+    timer_end(p, ST_BUILD, ev);
+    p->offsets_valid = true;
+  }
   if ((e = cudaStreamSynchronize(p->stream)) != cudaSuccess) return cuda_fail(e, "set_nodes sync");
   unsigned long long bad = *p->h_bad;
   if (bad != ~0ull) {
@@ -626,10 +632,15 @@ int bnfft_get_perm(const bnfft_plan_s* p, uint32_t* dev_out) {
   return e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "get_perm");
 }
 
-int bnfft_get_bin_offsets(const bnfft_plan_s* p, uint32_t* dev_out) {
+int bnfft_get_bin_offsets(bnfft_plan_s* p, uint32_t* dev_out) {
   if (!p || !dev_out) return BNFFT_E_INVALID_ARG;
   if (!p->nodes_set) return BNFFT_E_NODES_NOT_SET;
   cudaSetDevice(p->device);
+  if (!p->offsets_valid) {   // user-order plans build the key offsets on demand
+    cudaError_t eb = launch_build(p, nullptr, p->n);
+    if (eb != cudaSuccess) return cuda_fail(eb, "build kernel");
+    p->offsets_valid = true;
+  }
   cudaError_t e = cudaMemcpyAsync(dev_out, p->d_bin_start, (p->nkeys + 1) * sizeof(uint32_t),
                                   cudaMemcpyDeviceToDevice, p->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);

@@ -27,7 +27,9 @@ enum { BAD_NOT_FINITE = 1, BAD_RANGE = 2, BAD_BOX = 3 };
 // K1: validate + key.  bad = min over nodes of (index << 4 | code).
 __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams kp,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                            unsigned long long* __restrict__ bad) {
+                            unsigned long long* __restrict__ bad, double* __restrict__ xcopy) {
+  // xcopy != nullptr: the plan keeps the nodes in user order (d <= 2, user-blocked sort); the
+  // gather then reads xcopy[perm[i]] inside an L2-resident user block.
   // vals (identity permutation) is only written when no radix pass will run; the first pass
   // generates v = index itself.
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -37,6 +39,7 @@ __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams k
     bool nonfinite = false, range = false, box = false;
     for (int t = 0; t < kp.d; ++t) {
       double xv = x[i * kp.d + t];
+      if (xcopy) xcopy[i * kp.d + t] = xv;
       if (!isfinite(xv)) { nonfinite = true; continue; }
       if (!(xv >= -0.5 && xv < 0.5)) { range = true; continue; }
       if (kp.strict && !(xv >= kp.box_lo && xv <= kp.box_hi)) box = true;
@@ -82,11 +85,15 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(
   for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x) cnt[dgt] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kSortTile;
-#pragma unroll 4
+  uint32_t kk[kSortItems];
+#pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     int64_t idx = base + j * kSortThreads + threadIdx.x;
-    if (idx < n) atomicAdd(&cnt[(keys[idx] >> shift) & mask], 1u);   // integer counts: order-free
+    kk[j] = idx < n ? __ldg(&keys[idx]) : 0xffffffffu;
   }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j)   // integer counts: order-free
+    if (kk[j] != 0xffffffffu) atomicAdd(&cnt[(kk[j] >> shift) & mask], 1u);
   __syncthreads();
   for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x)
     hist[hist_index(sl, blockIdx.x, dgt, ndig)] = cnt[dgt];
@@ -178,8 +185,8 @@ __global__ void __launch_bounds__(256) scan_down_kernel(const uint32_t* __restri
   }
 }
 
-// K2b: stable scatter.  Warp w of the CTA owns tile elements [w*512, (w+1)*512), visited in
-// 16 rounds of 32 consecutive elements; ranks within the warp come from warp-private digit
+// K2b: stable scatter.  Warp w of the CTA owns tile elements [w*256, (w+1)*256), visited in
+// 8 rounds of 32 consecutive elements; ranks within the warp come from warp-private digit
 // counters (match_any groups equal digits in a round, lower lanes first), ranks across warps
 // from an exclusive prefix over the warp counters, ranks across tiles from the scanned
 // histogram.  Element order inside the tile is therefore preserved.  The tile is first reordered
@@ -190,12 +197,13 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift, int bits,
     const uint32_t* __restrict__ hist_scan, SegLayout sl) {
   constexpr int kWarps = kSortThreads / 32;
-  constexpr int kPerWarp = kSortTile / kWarps;   // 512
+  constexpr int kPerWarp = kSortTile / kWarps;   // 256
   __shared__ uint32_t wcnt[kWarps][1 << kMaxDigitBits];
   __shared__ uint32_t gbase[1 << kMaxDigitBits];
   __shared__ uint32_t tstart[1 << kMaxDigitBits];
-  __shared__ uint32_t skey[kSortTile];
-  __shared__ uint32_t sval[kSortTile];
+  extern __shared__ uint32_t sdyn[];      // skey[kSortTile], sval[kSortTile]
+  uint32_t* skey = sdyn;
+  uint32_t* sval = sdyn + kSortTile;
   __shared__ uint32_t wsum[kWarps];
   const int ndig = 1 << bits;
   const uint32_t mask = ndig - 1;
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   __syncthreads();
   // per digit: exclusive prefix over warps, tile count
   uint32_t tcount = 0;
-  const int dg0 = threadIdx.x;   // ndig <= 256 = blockDim
+  const int dg0 = threadIdx.x;   // ndig <= 256 <= blockDim
   if (dg0 < ndig) {
 #pragma unroll
     for (int ww = 0; ww < kWarps; ++ww) {
@@ -280,9 +288,10 @@ __global__ void build_kernel(const double* __restrict__ x, const uint32_t* __res
                              const uint32_t* __restrict__ skeys, double* __restrict__ xs,
                              uint32_t* __restrict__ key_start, int64_t n, int d, int64_t nbins,
                              int ub_log2, int64_t nkeys) {
+  // xs == nullptr: offsets only (plans that keep the nodes in user order)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < n) {
+    if (i < n && xs) {
       uint32_t j = perm[i];
       for (int t = 0; t < d; ++t) xs[i * d + t] = x[(int64_t)j * d + t];
     }
@@ -313,7 +322,8 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
   if (e != cudaSuccess) return e;
   if (n > 0) {
     keys_kernel<<<grid_for(n, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0,
-                                                         p->sort_passes ? nullptr : p->d_v0, p->d_bad);
+                                                         p->sort_passes ? nullptr : p->d_v0, p->d_bad,
+                                                         p->xs_user ? p->d_xs : nullptr);
     p->launches++;
   }
   return cudaGetLastError();
@@ -326,6 +336,11 @@ static cudaError_t exclusive_scan(bnfft_plan_s* p, const uint32_t* in, uint32_t*
   scan_down_kernel<<<(unsigned)nb, 256, 0, p->stream>>>(in, n, p->d_scan_part, out);
   p->launches += 3;
   return cudaGetLastError();
+}
+
+cudaError_t sort_prepare() {
+  return cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              2 * kSortTile * (int)sizeof(uint32_t));
 }
 
 cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
@@ -344,7 +359,8 @@ cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
       p->launches++;
       cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
       if (e != cudaSuccess) return e;
-      radix_scatter_kernel<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(
+      radix_scatter_kernel<<<(unsigned)sl.ntiles, kSortThreads, 2 * kSortTile * sizeof(uint32_t),
+                             p->stream>>>(
           kin, vin, kout, vout, n, shift, b, p->d_hist, sl);
       p->launches++;
       std::swap(kin, kout);
@@ -365,7 +381,8 @@ cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
 }
 
 cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n) {
-  build_kernel<<<grid_for(n + 1, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys, p->d_xs,
+  build_kernel<<<grid_for(n + 1, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys,
+                                                            p->xs_user ? nullptr : p->d_xs,
                                                             p->d_bin_start, n, p->opts.d,
                                                             p->nbins, p->ub_log2, p->nkeys);
   p->launches++;
