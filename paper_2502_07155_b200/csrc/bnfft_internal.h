@@ -16,6 +16,8 @@ constexpr int kGatherThreads = 256;   // nodes per gather CTA chunk (one node pe
 constexpr int kSortThreads = 512;
 constexpr int kSortItems = 8;         // keys per thread per tile
 constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kSortTileLog2 = 12;
+static_assert(kSortTile == (1 << kSortTileLog2), "sort tile is a power of two");
 constexpr int kMaxDigitBits = 8;
 constexpr int kQuadN = 64;            // Gauss-Legendre points for psi^ (reading A4)
 

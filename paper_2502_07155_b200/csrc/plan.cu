@@ -298,8 +298,9 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     int64_t gbytes_one = Ld * (int64_t)o->batch * (int64_t)p->csize;
     if (o->d <= 2 && gbytes_one <= ((int64_t)48 << 20)) {
       int64_t per = (int64_t)o->batch * (int64_t)p->csize;
-      int ub = 12;
+      int ub = kSortTileLog2;
       while (ub < 31 && (((int64_t)1 << (ub + 1)) * per) <= ((int64_t)16 << 20)) ++ub;
+      ub = std::max(ub, kSortTileLog2);   // user blocks are whole sort tiles
       p->ub_log2 = ub;
     } else {
       p->ub_log2 = 31;

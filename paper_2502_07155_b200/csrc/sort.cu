@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift, int bits,
     const uint32_t* __restrict__ hist_scan, SegLayout sl) {
   constexpr int kWarps = kSortThreads / 32;
-  constexpr int kPerWarp = kSortTile / kWarps;   // 256
+  constexpr int kPerWarp = kSortTile / kWarps;
   __shared__ uint32_t wcnt[kWarps][1 << kMaxDigitBits];
   __shared__ uint32_t gbase[1 << kMaxDigitBits];
   __shared__ uint32_t tstart[1 << kMaxDigitBits];
@@ -208,33 +208,39 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   const int ndig = 1 << bits;
   const uint32_t mask = ndig - 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kWarps * ndig; i += blockDim.x) wcnt[i / ndig][i % ndig] = 0;
-  for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x)
-    gbase[dgt] = hist_scan[hist_index(sl, blockIdx.x, dgt, ndig)];
+  for (int i = threadIdx.x; i < kWarps * (1 << kMaxDigitBits); i += kSortThreads)
+    if ((i & ((1 << kMaxDigitBits) - 1)) < ndig) (&wcnt[0][0])[i] = 0;
+  {
+    const int64_t h0 = hist_index(sl, blockIdx.x, 0, ndig);
+    const int64_t hs = hist_index(sl, blockIdx.x, 1, ndig) - h0;   // stride between digits
+    for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x) gbase[dgt] = hist_scan[h0 + dgt * hs];
+  }
   __syncthreads();
   const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
   const int tile_n = (int)min((int64_t)kSortTile, n - tbase);
-  const int64_t base = tbase + (int64_t)w * kPerWarp;
+  const uint32_t* __restrict__ kt = kin + tbase;          // tile-relative 32-bit indexing
+  const uint32_t* __restrict__ vt = vin ? vin + tbase : nullptr;
+  const int wbase = w * kPerWarp;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t k[kSortItems], v[kSortItems], r[kSortItems];
-  // all loads first (independent, in flight together), then the serial ranking rounds
+  // all loads first (independent, in flight together), then the ranking rounds
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    int64_t idx = base + j * 32 + lane;
-    bool valid = idx < n;
-    k[j] = valid ? __ldg(&kin[idx]) : 0u;
-    v[j] = valid ? (vin ? __ldg(&vin[idx]) : (uint32_t)idx) : 0u;
+    const int li = wbase + j * 32 + lane;
+    const bool valid = li < tile_n;
+    k[j] = valid ? __ldg(&kt[li]) : 0u;
+    v[j] = valid ? (vt ? __ldg(&vt[li]) : (uint32_t)(tbase + li)) : 0u;
   }
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    int64_t idx = base + j * 32 + lane;
-    bool valid = idx < n;
-    uint32_t dg = valid ? ((k[j] >> shift) & mask) : 0xffffffffu;
-    uint32_t peers = __match_any_sync(0xffffffffu, dg);
-    uint32_t cnt = valid ? wcnt[w][dg] : 0u;
+    const bool valid = wbase + j * 32 + lane < tile_n;
+    const uint32_t dg = valid ? ((k[j] >> shift) & mask) : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t cnt = valid ? wcnt[w][dg] : 0u;
     r[j] = cnt + __popc(peers & lt_mask);
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) wcnt[w][dg] = cnt + __popc(peers);
+    // every lane of the group stores the same new count (no leader election needed)
+    if (valid) wcnt[w][dg] = cnt + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
@@ -264,8 +270,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    int64_t idx = base + j * 32 + lane;
-    if (idx < n) {
+    if (wbase + j * 32 + lane < tile_n) {
       uint32_t dg = (k[j] >> shift) & mask;
       uint32_t lpos = tstart[dg] + wcnt[w][dg] + r[j];
       skey[lpos] = k[j];
@@ -348,7 +353,7 @@ cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
   if (n > 0 && p->sort_passes > 0) {
     SegLayout sl;
     sl.ntiles = (n + kSortTile - 1) / kSortTile;
-    sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - 12));
+    sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - kSortTileLog2));
     int bits = p->digit_bits;
     for (int pass = 0; pass < p->sort_passes; ++pass) {
       int shift = pass * bits;
