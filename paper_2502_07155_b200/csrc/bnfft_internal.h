@@ -1,6 +1,7 @@
 // Internal declarations of the bnfft library (product path).  Shares nothing with oracle/.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 #include <stdint.h>
@@ -125,7 +126,11 @@ struct bnfft_plan_s {
   int gather_bt = 1;          // batch slice per staged box
   int gather_smax = 1;        // segments (bins) staged per round
   int gather_box_cap = 0;     // d = 1: staged window capacity (complex elements)
-  int64_t gather_grid1 = 0;   // d = 1: persistent grid size (SMs x resident CTAs)
+  int64_t gather_grid1 = 0;   // persistent grid size (SMs x resident CTAs)
+  int gather_nslice = 1, gather_box_elems = 0, gather_bufstride = 0;
+  int gather_tbox[3] = {1, 1, 1};
+  alignas(64) CUtensorMap tmap;   // d >= 2: TMA descriptor of the theta grid (host copy)
+  CUtensorMap* d_tmap = nullptr;  // device (global memory) copy used by the kernel
   size_t gather_smem = 0;
 
   // timing

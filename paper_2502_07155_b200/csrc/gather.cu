@@ -1,11 +1,22 @@
 // Row a6 gather: host-side dispatch and launch (kernels in gather_impl.cuh).
+#include <cuda.h>
+
 #include <cstring>
 
 #include "gather_impl.cuh"
 
 namespace bnfft {
 
+const void* gather3c_kernel_p();
+const void* gather3c_kernel_e();
+
+// d = 3, m = 4, complex64: the warp-cooperative kernel (conflict-free shared-memory layout)
+static bool use_coop3(const bnfft_plan_s* p) {
+  return p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
+}
+
 static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false) {
+  if (d == 3 && m == 4 && !c128 && !batched) return poly ? gather3c_kernel_p() : gather3c_kernel_e();
   if (d == 1 && batched) return c128 ? gather_kernel_1d(m + 100, poly) : gather_kernel_1f(m + 100, poly);
   if (d == 1) return c128 ? gather_kernel_1d(m, poly) : gather_kernel_1f(m, poly);
   if (d == 2) return c128 ? gather_kernel_2d(m, poly) : gather_kernel_2f(m, poly);
@@ -30,6 +41,90 @@ size_t gather_box_elems(const bnfft_plan_s* p) {
 // Dynamic shared memory for staged boxes; the kernel also uses ~2 KB of static shared memory, and
 // the sum must stay under the 48 KB default (the attribute is raised only for single large boxes).
 static size_t smem_budget() { return 40u << 10; }
+
+// ---- d = 2, 3: TMA tensor map over theta and the binned persistent kernel
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
+  const int d = p->opts.d, T = 2 * p->opts.m;
+  // box extents per dim (dim 0 slowest); the innermost extent is padded to 16 bytes for TMA
+  int ext[3];
+  for (int t = 0; t < d; ++t) ext[t] = (1 << p->bin_log2[t]) + T - 1;
+  if (!p->c128) ext[d - 1] = (1 << p->bin_log2[d - 1]) + T;   // even start shift + 16-B multiple
+  if (use_coop3(p)) ext[d - 1] = kRow3;                       // conflict-free rows (bins 8x8x16)
+  size_t box_elems = 1;
+  for (int t = 0; t < d; ++t) box_elems *= (size_t)ext[t];
+  const size_t per = box_elems * p->csize;
+  const size_t budget = 48u << 10;              // bytes per staging buffer
+  int bt = (int)std::max<size_t>(1, std::min<size_t>((size_t)p->opts.batch, budget / per));
+  if (bt > 256) bt = 256;
+  const size_t buf_bytes = (per * bt + 127) & ~(size_t)127;
+  const int nbuf = use_coop3(p) ? 1 : 2;     // coop kernel: one box buffer, more CTAs per SM
+  p->gather_bt = bt;
+  p->gather_nslice = (p->opts.batch + bt - 1) / bt;
+  p->gather_box_elems = (int)box_elems;
+  p->gather_bufstride = (int)(buf_bytes / p->csize);
+  for (int t = 0; t < 3; ++t) p->gather_tbox[t] = t < d ? ext[t] : 1;
+  p->gather_smem = nbuf * buf_bytes;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, nsm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGatherThreads, p->gather_smem);
+  if (e != cudaSuccess) return e;
+  p->gather_grid1 = (int64_t)std::max(1, per_sm) * nsm;
+
+  // tensor map (innermost first): [re/im (c128)], z, y, (x), (batch)
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fp) return e != cudaSuccess ? e : cudaErrorNotSupported;
+  cuuint64_t gdim[5], gstr[4];
+  cuuint32_t box[5], estr[5];
+  int r = 0;
+  cuuint64_t stride = 8;
+  if (p->c128) {
+    gdim[r] = 2;
+    box[r] = 2;
+    ++r;
+    stride = 16;
+  }
+  for (int t = d - 1; t >= 0; --t) {
+    gdim[r] = (cuuint64_t)p->L;
+    box[r] = (cuuint32_t)ext[t];
+    ++r;
+  }
+  if (p->opts.batch > 1) {
+    gdim[r] = (cuuint64_t)p->opts.batch;
+    box[r] = (cuuint32_t)bt;
+    ++r;
+  }
+  // byte strides of dims 1..r-1
+  {
+    int k = 0;
+    cuuint64_t s = 8;                 // element = one double
+    if (p->c128) { gstr[k++] = 16; s = 16; }
+    (void)stride;
+    cuuint64_t acc = s;
+    for (int t = 0; t < d - 1; ++t) { acc *= (cuuint64_t)p->L; gstr[k++] = acc; }
+    if (p->opts.batch > 1) gstr[k++] = (cuuint64_t)p->Ld * p->csize;
+  }
+  for (int i = 0; i < r; ++i) estr[i] = 1;
+  CUresult cr = ((EncodeTiledFn)fp)(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)r, p->d_grid, gdim, gstr,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  if (!p->d_tmap) {
+    e = cudaMalloc((void**)&p->d_tmap, sizeof(CUtensorMap));
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaMemcpyAsync(p->d_tmap, &p->tmap, sizeof(CUtensorMap), cudaMemcpyHostToDevice, p->stream);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(p->stream);
+}
 constexpr int kMaxSegPerRound = 32;
 
 cudaError_t gather_prepare(bnfft_plan_s* p) {
@@ -51,6 +146,7 @@ cudaError_t gather_prepare(bnfft_plan_s* p) {
     p->gather_grid1 = (int64_t)std::max(1, per_sm) * nsm;
     return cudaSuccess;
   }
+  if (p->opts.d >= 2) return gatherN_prepare(p, fn);
   size_t per = gather_box_elems(p) * p->csize;
   int bt = (int)std::max<size_t>(1, std::min<size_t>((size_t)p->opts.batch, smem_budget() / per));
   p->gather_bt = bt;
@@ -101,6 +197,19 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
       }
   }
   void* args[] = {&gp};
+  gp.key_start = p->d_bin_start;
+  gp.nkeys = p->nkeys;
+  gp.nslice = p->gather_nslice;
+  gp.bufstride = p->gather_bufstride;
+  for (int t = 0; t < 3; ++t) gp.tbox[t] = p->gather_tbox[t];
+  if (p->opts.d >= 2) {
+    gp.box_elems = p->gather_box_elems;
+    void* args2[] = {&gp, &p->d_tmap};
+    unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p->gather_grid1, p->nkeys));
+    cudaError_t e2 = cudaLaunchKernel(fn, dim3(nb), dim3(kGatherThreads), args2, p->gather_smem, p->stream);
+    p->launches++;
+    return e2;
+  }
   unsigned blocks;
   if (p->opts.d == 1 && p->opts.batch == 1) {
     const int64_t ch = (int64_t)kGatherThreads * NPT1<R>::v;

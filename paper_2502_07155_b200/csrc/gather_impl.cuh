@@ -24,6 +24,8 @@
 // node's (2m)^d taps from its segment's box in a fixed order (bitwise reproducible) and writes f
 // to the user position perm[i].
 #pragma once
+#include <cuda.h>
+
 #include <algorithm>
 
 #include "bnfft_internal.h"
@@ -61,6 +63,11 @@ struct GatherParams {
   R inv_m;
   int boxcap;             // d = 1 kernel: staged-box capacity in complex elements
   int xs_user;            // xs in user order: node i of the sorted order is xs[perm[i]]
+  const uint32_t* key_start;   // binned kernel: first sorted position of each (user block, bin)
+  int64_t nkeys;
+  int tbox[3];            // binned kernel: TMA box extents per dim (dim 0 slowest), innermost padded
+  int nslice;             // batch slices per unit (bt spectra each)
+  int bufstride;          // binned kernel: elements between the two staging buffers (128-B aligned)
   WinParams wp;
   alignas(16) R ceo[PolyH<R>::NH][kMaxTaps / 2][2];   // [k][i][0] = E_i coeff k, [k][i][1] = O_i
 };
@@ -573,11 +580,304 @@ __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_co
 
 // D == 1: the pipelined window kernel (batch == 1) or, for batched d = 1 plans, the generic
 // segment kernel (returned for m + 100).
+// d = 2, 3 gather: persistent CTAs over the sort keys (user block, bin), TMA tensor staging.
+//
+// Work item = (key u, batch slice s).  The bin's grid neighbourhood (bin + (m-1, m) halo) is one box
+// of the theta tensor; cp.async.bulk.tensor copies it into shared memory with out-of-bound elements
+// zero-filled by the TMA unit (zero extension outside I_L, reading A5).  Items are double-buffered:
+// the box of the CTA's next item is in flight while the current one is contracted.  The nodes of
+// the key are processed 256 at a time; each thread evaluates its node's tap polynomials (all dims)
+// and contracts the (2m)^d taps from shared memory in a fixed order.
+__device__ __forceinline__ void tma_load_box(const CUtensorMap* tm, void* dst, uint64_t* bar, int rank,
+                                             const int* c) {
+  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+  const uint64_t t = reinterpret_cast<uint64_t>(tm);
+  if (rank == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(d), "l"(t), "r"(b), "r"(c[0]), "r"(c[1]) : "memory");
+  else if (rank == 3)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(d), "l"(t), "r"(b), "r"(c[0]), "r"(c[1]), "r"(c[2]) : "memory");
+  else if (rank == 4)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+        ::"r"(d), "l"(t), "r"(b), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+        ::"r"(d), "l"(t), "r"(b), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+}
+
+// Issue the box of item (u, s) (thread 0 only).  The tensor map lives in global memory (written once
+// at plan creation).  Tensor coordinates are innermost first; complex128
+// adds an innermost dimension of 2 doubles; batch is the outermost dimension.
+template <int D, typename R>
+__device__ __forceinline__ void issue_box(const GatherParams<R>& p, const CUtensorMap* tm, int64_t u, int sl,
+                                          void* dst, uint64_t* bar, uint32_t bytes) {
+  int64_t nbins = 1;
+#pragma unroll
+  for (int t = 0; t < D; ++t) nbins *= p.nb[t];
+  uint32_t rem = (uint32_t)(u % nbins);
+  int org[3];
+#pragma unroll
+  for (int t = D - 1; t >= 0; --t) {
+    const uint32_t bt = rem % (uint32_t)p.nb[t];
+    rem /= (uint32_t)p.nb[t];
+    org[t] = (int)((int64_t)bt << p.log2W[t]) - (p.wp.m - 1);
+  }
+  // the innermost box start must be 16-byte aligned: complex64 boxes start at an even z (the box
+  // is one element wider than the halo needs; the kernel adds the shift back)
+  if (sizeof(R) == 4) org[D - 1] &= ~1;
+  int c[5];
+  int r = 0;
+  if (sizeof(R) == 8) c[r++] = 0;                // complex128: re/im pair
+#pragma unroll
+  for (int t = D - 1; t >= 0; --t) c[r++] = org[t];
+  if (p.batch > 1) c[r++] = sl * p.bt;
+  mbar_expect_tx(bar, bytes);
+  tma_load_box(tm, dst, bar, r, c);
+}
+
+template <int D, int T, typename R, bool POLY>
+__global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_constant__ GatherParams<R> p,
+                                                                 const CUtensorMap* __restrict__ tmap) {
+  using C = typename CT<R>::C;
+  constexpr int m = T / 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const int BZ = p.tbox[D - 1];                      // innermost (padded) extent
+  const int BY = D == 3 ? p.tbox[1] : 1;
+  const int box_elems = p.box_elems;                 // per spectrum (with padding)
+  const uint32_t buf_elems = (uint32_t)box_elems * p.bt;
+  C* const buf0 = reinterpret_cast<C*>(smem_raw);
+  const uint32_t bytes = buf_elems * (uint32_t)sizeof(C);
+  const int64_t G = gridDim.x;
+  const int nsl = p.nslice;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  C* __restrict__ out = (C*)p.out;
+
+  // the CTA's item sequence: keys u = blockIdx.x + j*G (non-empty ones), slices 0..nsl-1 each
+  auto next_key = [&](int64_t u) -> int64_t {
+    while (u < p.nkeys && __ldg(&p.key_start[u + 1]) == __ldg(&p.key_start[u])) u += G;
+    return u;
+  };
+  int64_t u = next_key(blockIdx.x);
+  int sl = 0;
+  if (u >= p.nkeys) return;
+  if (threadIdx.x == 0) issue_box<D, R>(p, tmap, u, 0, buf0, &bars[0], bytes);
+  uint32_t phases = 0u;
+  for (int it = 0;; ++it) {
+    const int b = it & 1;
+    // next item
+    int64_t un = u;
+    int sn = sl + 1;
+    if (sn == nsl) {
+      sn = 0;
+      un = next_key(u + G);
+    }
+    if (un < p.nkeys && threadIdx.x == 0)
+      issue_box<D, R>(p, tmap, un, sn, buf0 + (b ^ 1) * p.bufstride, &bars[b ^ 1], bytes);
+    mbar_wait(&bars[b], (phases >> b) & 1u);
+    phases ^= 1u << b;
+    const C* box = buf0 + b * p.bufstride;
+    // bin origin (cells) of key u
+    int64_t nbins = 1;
+#pragma unroll
+    for (int t = 0; t < D; ++t) nbins *= p.nb[t];
+    uint32_t rem = (uint32_t)(u % nbins);
+    int bo[3];
+#pragma unroll
+    for (int t = D - 1; t >= 0; --t) {
+      const uint32_t bt = rem % (uint32_t)p.nb[t];
+      rem /= (uint32_t)p.nb[t];
+      bo[t] = (int)(bt << p.log2W[t]);
+    }
+    const int64_t i_beg = __ldg(&p.key_start[u]), i_end = __ldg(&p.key_start[u + 1]);
+    const int nbt = min(p.bt, p.batch - sl * p.bt);
+    for (int64_t i = i_beg + threadIdx.x; i < i_end; i += kGatherThreads) {
+      const uint32_t dst = __ldg(&p.perm[i]);
+      const int64_t src = p.xs_user ? (int64_t)dst : i;
+      int off[3];
+      R w[D][T];
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        const double Lx = __dmul_rn(p.Lf, __ldg(&p.xs[src * D + t]));
+        const double fl = floor(Lx);
+        double uu = Lx - fl;
+        int64_t c = (int64_t)fl + p.L / 2;
+        if (c > p.L - 1) { c = p.L - 1; uu = 1.0; }
+        off[t] = (int)c - bo[t];
+        if (sizeof(R) == 4 && t == D - 1) off[t] += (bo[t] - (m - 1)) & 1;   // even-aligned box start
+        const DimState<R> st = dim_state<T, R, POLY>(uu, p);
+        all_taps<T, POLY>(st, p, w[t]);
+      }
+      for (int bb = 0; bb < nbt; ++bb) {
+        const C* bx = box + bb * box_elems;
+        C acc = czero<C>();
+        if (D == 2) {
+#pragma unroll
+          for (int a = 0; a < T; ++a) {
+            const C* row = bx + (off[0] + a) * BZ + off[1];
+            C racc = czero<C>();
+#pragma unroll
+            for (int k = 0; k < T; ++k) cmac(racc, w[1][k], row[k]);
+            cmac(acc, w[0][a], racc);
+          }
+        } else {
+#pragma unroll 1
+          for (int a = 0; a < T; ++a) {
+            const C* plane = bx + (off[0] + a) * BY * BZ;
+            C pacc = czero<C>();
+#pragma unroll
+            for (int bq = 0; bq < T; ++bq) {
+              const C* row = plane + (off[1] + bq) * BZ + off[2];
+              C racc = czero<C>();
+#pragma unroll
+              for (int k = 0; k < T; ++k) cmac(racc, w[2][k], row[k]);
+              cmac(pacc, w[1][bq], racc);
+            }
+            R wa = w[0][0];
+#pragma unroll
+            for (int q = 1; q < T; ++q) wa = (a == q) ? w[0][q] : wa;
+            cmac(acc, wa, pacc);
+          }
+        }
+        out[(int64_t)(sl * p.bt + bb) * p.n + dst] = acc;
+      }
+    }
+    if (un >= p.nkeys) break;
+    __syncthreads();   // everyone done with buffer b before it is refilled (item after next)
+    u = un;
+    sl = sn;
+  }
+}
+
+// d = 3, m = 4, complex64, batch 1: half-warp-cooperative contraction (TMA staging as gatherN).
+//
+// With one node per thread, the 32 lanes of a warp read 32 unrelated rows of the box: random
+// 8-byte shared-memory accesses with ~4-way bank conflicts.  Here each half-warp contracts one
+// node: lane (r, c) = ((lane >> 3) & 1, lane & 7) reads z index c of rows b = 2k + r, k < 4, of every
+// x-plane.  The box rows hold kRow3 = 24 elements (192 B; bins are 8 x 8 x 16 cells, so 16 + 2m = 24
+// is exactly the halo extent), which puts rows b and b+1 16 banks apart: each half-warp phase of an
+// LDS.64 reads two conflict-free 64-byte rows, 2 wavefronts per instruction (the minimum).  Lanes
+// first prepare 32 nodes (cells, the 24 tap weights) into a per-warp stash; then the half-warps
+// contract the stashed nodes pairwise and reduce over their 16 lanes with shuffles.
+constexpr int kRow3 = 24;
+
+template <bool POLY>
+__global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_constant__ GatherParams<float> p,
+                                                                  const CUtensorMap* __restrict__ tmap) {
+  using C = float2;
+  constexpr int T = 8, m = 4, D = 3;
+  constexpr int kW = kGatherThreads / 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[1];
+  __shared__ float s_w[kW][32][3 * T];          // tap weights per stashed node
+  __shared__ int s_off[kW][32][3];
+  __shared__ uint32_t s_dst[kW][32];
+  const int BZ = kRow3, BY = p.tbox[1];
+  const int box_elems = p.box_elems;
+  const uint32_t bytes = (uint32_t)box_elems * (uint32_t)sizeof(C);
+  C* const box = reinterpret_cast<C*>(smem_raw);
+  const int64_t G = gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int hw = lane >> 4, rr = (lane >> 3) & 1, cz = lane & 7;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  C* __restrict__ out = (C*)p.out;
+  uint32_t phase = 0u;
+  for (int64_t u = blockIdx.x; u < p.nkeys; u += G) {
+    const int64_t i_beg = __ldg(&p.key_start[u]), i_end = __ldg(&p.key_start[u + 1]);
+    if (i_beg == i_end) continue;
+    if (threadIdx.x == 0) issue_box<D, float>(p, tmap, u, 0, box, &bars[0], bytes);
+    // bin origin (cells)
+    const int64_t nbins = p.nb[0] * p.nb[1] * p.nb[2];
+    uint32_t rem = (uint32_t)(u % nbins);
+    int bo[3];
+#pragma unroll
+    for (int t = D - 1; t >= 0; --t) {
+      const uint32_t btc = rem % (uint32_t)p.nb[t];
+      rem /= (uint32_t)p.nb[t];
+      bo[t] = (int)(btc << p.log2W[t]);
+    }
+    const int zshift = (bo[2] - (m - 1)) & 1;      // even-aligned box start (issue_box)
+    bool waited = false;
+    for (int64_t g0 = i_beg + (int64_t)wid * 32; g0 < i_end; g0 += kGatherThreads) {
+      // ---- stash: lane prepares node g0 + lane (overlaps the TMA of the box)
+      const int nn = (int)min((int64_t)32, i_end - g0);
+      if (lane < nn) {
+        const int64_t i = g0 + lane;
+        const uint32_t dst = __ldg(&p.perm[i]);
+        const int64_t src = p.xs_user ? (int64_t)dst : i;
+        s_dst[wid][lane] = dst;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+          const double Lx = __dmul_rn(p.Lf, __ldg(&p.xs[src * D + t]));
+          const double fl = floor(Lx);
+          double uu = Lx - fl;
+          int64_t c = (int64_t)fl + p.L / 2;
+          if (c > p.L - 1) { c = p.L - 1; uu = 1.0; }
+          int o = (int)c - bo[t];
+          if (t == D - 1) o += zshift;
+          s_off[wid][lane][t] = o;
+          const DimState<float> st = dim_state<T, float, POLY>(uu, p);
+          float w[T];
+          all_taps<T, POLY>(st, p, w);
+#pragma unroll
+          for (int k = 0; k < T; ++k) s_w[wid][lane][t * T + k] = w[k];
+        }
+      }
+      __syncwarp();
+      if (!waited) {
+        mbar_wait(&bars[0], phase);
+        waited = true;
+      }
+      // ---- contract stashed nodes two at a time (half-warp hw takes node q + hw)
+      for (int q0 = 0; q0 < nn; q0 += 2) {
+        const int q = min(q0 + hw, nn - 1);
+        const int o0 = s_off[wid][q][0], o1 = s_off[wid][q][1], o2 = s_off[wid][q][2];
+        const C* bx = box + ((o0 * BY + o1 + rr) * BZ + o2 + cz);
+        C acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int a = 0; a < T; ++a) {
+          const C* pl = bx + a * BY * BZ;
+          C t = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < T / 2; ++k) cmac(t, s_w[wid][q][T + 2 * k + rr], pl[2 * k * BZ]);
+          cmac(acc, s_w[wid][q][a], t);
+        }
+        const float wz = s_w[wid][q][2 * T + cz];
+        acc = __fmul2_rn(make_float2(wz, wz), acc);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        }
+        if ((lane & 15) == 0 && q0 + hw < nn) out[s_dst[wid][q]] = acc;
+      }
+      __syncwarp();
+    }
+    if (!waited) mbar_wait(&bars[0], phase);   // warps without nodes still consume the phase
+    phase ^= 1u;
+    __syncthreads();   // box free before the next item's TMA
+  }
+}
+
 template <int D, typename R, bool POLY, int MM>
 static const void* kernel_for(int m) {
   if (m == MM) {
     if constexpr (D == 1) return (const void*)gather1_kernel<2 * MM, R, POLY>;
-    else return (const void*)gather_kernel<D, 2 * MM, R, POLY>;
+    else return (const void*)gatherN_kernel<D, 2 * MM, R, POLY>;
   }
   if constexpr (D == 1) {
     if (m == MM + 100) return (const void*)gather_kernel<1, 2 * MM, R, POLY>;

@@ -182,6 +182,7 @@ int bnfft_destroy(bnfft_plan_s* p) {
   dfree(p->d_x_stage);
   dfree(p->d_fhat_stage);
   dfree(p->d_f_stage);
+  dfree(p->d_tmap);
   free_nodes(p);
   if (p->h_bad) cudaFreeHost(p->h_bad);
   for (auto& t : p->pending) {
@@ -282,8 +283,11 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   while (((int64_t)1 << (lgL + 1)) <= L) ++lgL;
   lg = std::min(lg, lgL);
   int64_t nbins = 1;
+  // d = 3, m = 4, complex64, batch 1 (warp-cooperative gather): bins of 8 x 8 x 16 cells, so the
+  // innermost box extent 16 + 2m = 24 gives conflict-free shared-memory rows.
+  const bool coop3 = o->d == 3 && o->m == 4 && o->prec == BNFFT_C64 && o->batch == 1 && lgL >= 4;
   for (int t = 0; t < 3; ++t) {
-    p->bin_log2[t] = t < o->d ? lg : 0;
+    p->bin_log2[t] = t < o->d ? ((coop3 && t == 2) ? 4 : lg) : 0;
     p->nb_dim[t] = t < o->d ? (L + (1 << lg) - 1) >> lg : 1;
     nbins *= p->nb_dim[t];
   }
@@ -459,7 +463,7 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
   if ((e = launch_sort(p, n)) != cudaSuccess) return cuda_fail(e, "sort kernels");
   timer_end(p, ST_SORT, ev);
   p->offsets_valid = false;
-  if (!p->xs_user) {
+  if (!p->xs_user || p->opts.d >= 2) {   // sorted node copy and/or key offsets (binned gather)
     timer_begin(p, ST_BUILD, &ev);
     if ((e = launch_build(p, x, n)) != cudaSuccess) return cuda_fail(e, "build kernel");
     timer_end(p, ST_BUILD, ev);
