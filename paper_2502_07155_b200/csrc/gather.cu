@@ -204,6 +204,13 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
   for (int t = 0; t < 3; ++t) gp.tbox[t] = p->gather_tbox[t];
   if (p->opts.d >= 2) {
     gp.box_elems = p->gather_box_elems;
+    {
+      int mb = 0;
+      int64_t mx = std::max(p->nb_dim[0], std::max(p->nb_dim[1], p->nb_dim[2]));
+      while (((int64_t)1 << mb) < mx) ++mb;
+      gp.morton_bits = mb;
+      gp.nkeys_morton = (p->nkeys / p->nbins) << (3 * mb);
+    }
     void* args2[] = {&gp, &p->d_tmap};
     unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p->gather_grid1, p->nkeys));
     cudaError_t e2 = cudaLaunchKernel(fn, dim3(nb), dim3(kGatherThreads), args2, p->gather_smem, p->stream);

@@ -68,6 +68,8 @@ struct GatherParams {
   int tbox[3];            // binned kernel: TMA box extents per dim (dim 0 slowest), innermost padded
   int nslice;             // batch slices per unit (bt spectra each)
   int bufstride;          // binned kernel: elements between the two staging buffers (128-B aligned)
+  int morton_bits;        // d = 3 cooperative kernel: bits per bin coordinate of the Z-order walk
+  int64_t nkeys_morton;   // user blocks x 8^morton_bits
   WinParams wp;
   alignas(16) R ceo[PolyH<R>::NH][kMaxTaps / 2][2];   // [k][i][0] = E_i coeff k, [k][i][1] = O_i
 };
@@ -759,6 +761,23 @@ __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_co
   }
 }
 
+// Morton (Z-order) index v -> row-major bin key (or -1 when the decoded bin lies outside the bin
+// grid, which is padded to powers of two for the interleaving); user block = v >> 3*mbits.
+__device__ __forceinline__ int64_t morton_key3(int64_t v, const GatherParams<float>& p) {
+  const int mb = p.morton_bits;
+  const int64_t blk = v >> (3 * mb);
+  uint32_t c[3] = {0u, 0u, 0u};
+  uint32_t vv = (uint32_t)(v & ((1ll << (3 * mb)) - 1));
+  for (int bit = 0; bit < mb; ++bit) {
+    c[2] |= ((vv >> (3 * bit)) & 1u) << bit;
+    c[1] |= ((vv >> (3 * bit + 1)) & 1u) << bit;
+    c[0] |= ((vv >> (3 * bit + 2)) & 1u) << bit;
+  }
+  if (c[0] >= (uint32_t)p.nb[0] || c[1] >= (uint32_t)p.nb[1] || c[2] >= (uint32_t)p.nb[2]) return -1;
+  const int64_t nbins = p.nb[0] * p.nb[1] * p.nb[2];
+  return blk * nbins + ((int64_t)c[0] * p.nb[1] + c[1]) * p.nb[2] + c[2];
+}
+
 // d = 3, m = 4, complex64, batch 1: half-warp-cooperative contraction (TMA staging as gatherN).
 //
 // With one node per thread, the 32 lanes of a warp read 32 unrelated rows of the box: random
@@ -779,9 +798,10 @@ __global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_c
   constexpr int kW = kGatherThreads / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[1];
-  __shared__ float s_w[kW][32][3 * T];          // tap weights per stashed node
-  __shared__ int s_off[kW][32][3];
-  __shared__ uint32_t s_dst[kW][32];
+  // per stashed node: x weights [0,8), y weights split by parity [8,16) = (w_y[0], w_y[2], w_y[4],
+  // w_y[6], w_y[1], ...), z weights [16,24); offsets + destination as one int4
+  __shared__ __align__(16) float s_w[kW][32][3 * T];
+  __shared__ __align__(16) int4 s_od[kW][32];
   const int BZ = kRow3, BY = p.tbox[1];
   const int box_elems = p.box_elems;
   const uint32_t bytes = (uint32_t)box_elems * (uint32_t)sizeof(C);
@@ -796,7 +816,12 @@ __global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_c
   __syncthreads();
   C* __restrict__ out = (C*)p.out;
   uint32_t phase = 0u;
-  for (int64_t u = blockIdx.x; u < p.nkeys; u += G) {
+  // keys visited in Morton (Z) order of the bin coordinates, so that the bins in flight at one time
+  // form a compact 3-D block and their halos are served from L2
+  const int64_t nvirt = p.nkeys_morton;
+  for (int64_t v = blockIdx.x; v < nvirt; v += G) {
+    const int64_t u = morton_key3(v, p);
+    if (u < 0) continue;
     const int64_t i_beg = __ldg(&p.key_start[u]), i_end = __ldg(&p.key_start[u + 1]);
     if (i_beg == i_end) continue;
     if (threadIdx.x == 0) issue_box<D, float>(p, tmap, u, 0, box, &bars[0], bytes);
@@ -819,7 +844,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_c
         const int64_t i = g0 + lane;
         const uint32_t dst = __ldg(&p.perm[i]);
         const int64_t src = p.xs_user ? (int64_t)dst : i;
-        s_dst[wid][lane] = dst;
+        int od[3];
 #pragma unroll
         for (int t = 0; t < D; ++t) {
           const double Lx = __dmul_rn(p.Lf, __ldg(&p.xs[src * D + t]));
@@ -829,13 +854,20 @@ __global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_c
           if (c > p.L - 1) { c = p.L - 1; uu = 1.0; }
           int o = (int)c - bo[t];
           if (t == D - 1) o += zshift;
-          s_off[wid][lane][t] = o;
+          od[t] = o;
           const DimState<float> st = dim_state<T, float, POLY>(uu, p);
           float w[T];
           all_taps<T, POLY>(st, p, w);
-#pragma unroll
-          for (int k = 0; k < T; ++k) s_w[wid][lane][t * T + k] = w[k];
+          float4* sw = reinterpret_cast<float4*>(&s_w[wid][lane][t * T]);
+          if (t == 1) {
+            sw[0] = make_float4(w[0], w[2], w[4], w[6]);
+            sw[1] = make_float4(w[1], w[3], w[5], w[7]);
+          } else {
+            sw[0] = make_float4(w[0], w[1], w[2], w[3]);
+            sw[1] = make_float4(w[4], w[5], w[6], w[7]);
+          }
         }
+        s_od[wid][lane] = make_int4(od[0], od[1], od[2], (int)dst);
       }
       __syncwarp();
       if (!waited) {
@@ -845,16 +877,21 @@ __global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_c
       // ---- contract stashed nodes two at a time (half-warp hw takes node q + hw)
       for (int q0 = 0; q0 < nn; q0 += 2) {
         const int q = min(q0 + hw, nn - 1);
-        const int o0 = s_off[wid][q][0], o1 = s_off[wid][q][1], o2 = s_off[wid][q][2];
-        const C* bx = box + ((o0 * BY + o1 + rr) * BZ + o2 + cz);
+        const int4 od = s_od[wid][q];
+        const float4 wx0 = *reinterpret_cast<const float4*>(&s_w[wid][q][0]);
+        const float4 wx1 = *reinterpret_cast<const float4*>(&s_w[wid][q][4]);
+        const float4 wy = *reinterpret_cast<const float4*>(&s_w[wid][q][T + 4 * rr]);
+        const float wxa[T] = {wx0.x, wx0.y, wx0.z, wx0.w, wx1.x, wx1.y, wx1.z, wx1.w};
+        const float wyk[T / 2] = {wy.x, wy.y, wy.z, wy.w};
+        const C* bx = box + ((od.x * BY + od.y + rr) * BZ + od.z + cz);
         C acc = make_float2(0.f, 0.f);
 #pragma unroll
         for (int a = 0; a < T; ++a) {
           const C* pl = bx + a * BY * BZ;
           C t = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int k = 0; k < T / 2; ++k) cmac(t, s_w[wid][q][T + 2 * k + rr], pl[2 * k * BZ]);
-          cmac(acc, s_w[wid][q][a], t);
+          for (int k = 0; k < T / 2; ++k) cmac(t, wyk[k], pl[2 * k * BZ]);
+          cmac(acc, wxa[a], t);
         }
         const float wz = s_w[wid][q][2 * T + cz];
         acc = __fmul2_rn(make_float2(wz, wz), acc);
@@ -863,7 +900,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_c
           acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
           acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
         }
-        if ((lane & 15) == 0 && q0 + hw < nn) out[s_dst[wid][q]] = acc;
+        if ((lane & 15) == 0 && q0 + hw < nn) out[(uint32_t)od.w] = acc;
       }
       __syncwarp();
     }
