@@ -34,6 +34,17 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
+
+
+def gather_kernel_name(cfg, prec):
+    """The gather kernel the library dispatches for this workload (gather.cu select_kernel)."""
+    if cfg.d == 1:
+        return "bnfft::gather1_kernel" if cfg.batch == 1 else "bnfft::gather_kernel"
+    if cfg.d == 3 and cfg.m == 4 and prec == "c64" and cfg.batch == 1:
+        return "bnfft::gather3c_kernel"
+    return "bnfft::gatherN_kernel"
+
+
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
 
 
@@ -229,6 +240,7 @@ def run_gpu(args):
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     from paper_2502_07155_b200 import bnfft as bn
+    from paper_2502_07155_b200 import shard
 
     cfg, prec, window = workload(args)
     dev = torch.device("cuda", local)
@@ -238,13 +250,13 @@ def run_gpu(args):
     x_dev = torch.from_numpy(x_np).to(dev)
     fh_dev = torch.from_numpy(fh_np).to(dev)
 
+    sampler = ClockSampler(local)
+    sampler.start()        # samples from the warm-up on, through the timed region
     plan, out, step, e0, e1 = time_variant(torch, bn, cfg, prec, window, x_dev, fh_dev,
                                            args.steps, args.warmup, stream, local)
-    sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
     e0.record(stream)
     for _ in range(args.steps):
         step()
@@ -253,11 +265,7 @@ def run_gpu(args):
     clocks = sampler.stop()
     if world > 1:
         dist.barrier()
-    ms_total = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = shard.max_over_ranks(e0.elapsed_time(e1), device=dev)
     ms_step = ms_total / args.steps
     tm = plan.timing()
     info = plan.info()
@@ -265,7 +273,7 @@ def run_gpu(args):
     stages = {k: getattr(tm, "ms_" + k) / K for k in
               ("psihat", "keys", "sort", "build", "deconv", "fft", "gather")}
     launches = int(tm.kernel_launches)
-    value = cfg.N * cfg.batch * world / (ms_step * 1e-3)
+    value = shard.aggregate_rate(cfg.N * cfg.batch, world, ms_step)
 
     line = None
     if rank == 0:
@@ -287,7 +295,7 @@ def run_gpu(args):
             "vs_baseline": None, "dtype": "f64" if prec == "c128" else "f32",
             "data": "synthetic (seeded, synth/; BASELINE configs recipe)",
             "config": dict(describe(cfg, prec, window), parallelism=f"replicas{world}"),
-            "roofline": {"bound": "hbm", "kernel": "gather (bnfft::gather_kernel)",
+            "roofline": {"bound": "hbm", "kernel": gather_kernel_name(cfg, prec),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "bytes_per_node": bpn, "peak_source": hbm_src,
@@ -319,13 +327,9 @@ def run_gpu(args):
             plan.transform_host(xh, fhh, fo)
         b.record(stream)
         torch.cuda.synchronize()
-        ems = a.elapsed_time(b) / K
-        if world > 1:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = shard.max_over_ranks(a.elapsed_time(b) / K, device=dev)
         if rank == 0:
-            line["e2e"] = {"value": cfg.N * cfg.batch * world / (ems * 1e-3), "unit": "nodes/s",
+            line["e2e"] = {"value": shard.aggregate_rate(cfg.N * cfg.batch, world, ems), "unit": "nodes/s",
                            "ms_per_step": ems,
                            "h2d_bytes_per_step": int(xh.numel() * 8 + fhh.numel() * fhh.element_size()),
                            "d2h_bytes_per_step": int(fo.numel() * fo.element_size()),

@@ -294,3 +294,26 @@ def test_reset_nodes_grow_and_shrink(bn, torch):
         f = plan.execute(ft).cpu().numpy()
         assert rel_l2(f, O.algorithm2(x, fh.astype(np.complex128), 64, 2.0, 6)["f"]) <= 1e-5
     plan.close()
+
+
+@pytest.mark.parametrize("cid,d,M,N,prec", [(2, 1, 1 << 12, 100_001, "c64"), (3, 2, 128, 40_000, "c128"),
+                                           (4, 3, 32, 30_000, "c64")])
+def test_shards_bitwise(bn, torch, cid, d, M, N, prec):
+    """Node sharding (the multi-GPU layout): plans over disjoint node shards with the
+    same spectrum reproduce the single-plan result bitwise (per-node work is independent)."""
+    from paper_2502_07155_b200 import shard
+    cfg = synth.CONFIGS[cid].scaled(d=d, M=M, N=N)
+    x = torch.from_numpy(synth.make_nodes(cfg, variant=9)).cuda()
+    fh = torch.from_numpy(synth.make_spectrum(cfg, variant=9, prec=prec)).cuda()
+    full = bn.Plan(d, M, 2.0, cfg.m, "sinh", prec)
+    full.set_nodes(x)
+    ref = full.execute(fh).clone()
+    parts = []
+    for r in range(3):
+        a, b = shard.node_shard(N, r, 3)
+        p = bn.Plan(d, M, 2.0, cfg.m, "sinh", prec)
+        p.set_nodes(x[a:b].contiguous())
+        parts.append(p.execute(fh).clone())
+        p.close()
+    assert torch.equal(torch.cat(parts, dim=1), ref)
+    full.close()
