@@ -185,6 +185,18 @@ __global__ void __launch_bounds__(256) scan_down_kernel(const uint32_t* __restri
   }
 }
 
+// Lanes of the warp holding the same digit (including the caller), by intersecting one ballot per
+// digit bit (cheaper than MATCH.ANY); invalid lanes (tile tail) form their own group.
+__device__ __forceinline__ uint32_t peers_by_ballot(uint32_t dg, int bits, bool valid) {
+  uint32_t peers = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return ~peers;
+  for (int b = 0; b < bits; ++b) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, (dg >> b) & 1u);
+    peers &= ((dg >> b) & 1u) ? bal : ~bal;
+  }
+  return peers;
+}
+
 // K2b: stable scatter.  Warp w of the CTA owns tile elements [w*256, (w+1)*256), visited in
 // 8 rounds of 32 consecutive elements; ranks within the warp come from warp-private digit
 // counters (match_any groups equal digits in a round, lower lanes first), ranks across warps
@@ -235,7 +247,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   for (int j = 0; j < kSortItems; ++j) {
     const bool valid = wbase + j * 32 + lane < tile_n;
     const uint32_t dg = valid ? ((k[j] >> shift) & mask) : 0xffffffffu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t peers = peers_by_ballot(dg, bits, valid);
     const uint32_t cnt = valid ? wcnt[w][dg] : 0u;
     r[j] = cnt + __popc(peers & lt_mask);
     __syncwarp();
