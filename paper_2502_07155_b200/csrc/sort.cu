@@ -187,14 +187,18 @@ __global__ void __launch_bounds__(256) scan_down_kernel(const uint32_t* __restri
 
 // Lanes of the warp holding the same digit (including the caller), by intersecting one ballot per
 // digit bit (cheaper than MATCH.ANY); invalid lanes (tile tail) form their own group.
-__device__ __forceinline__ uint32_t peers_by_ballot(uint32_t dg, int bits, bool valid) {
-  uint32_t peers = __ballot_sync(0xffffffffu, valid);
-  if (!valid) return ~peers;
-  for (int b = 0; b < bits; ++b) {
-    const uint32_t bal = __ballot_sync(0xffffffffu, (dg >> b) & 1u);
-    peers &= ((dg >> b) & 1u) ? bal : ~bal;
+// Every lane executes every ballot (no early exit: the full-mask ballots need all 32 lanes).
+template <int BITS>
+__device__ __forceinline__ uint32_t peers_by_ballot(uint32_t dg, bool valid) {
+  const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+  uint32_t peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const uint32_t bit = (dg >> b) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+    peers &= ~(bal ^ (0u - bit));          // bit ? bal : ~bal
   }
-  return peers;
+  return valid ? (peers & vmask) : ~vmask;
 }
 
 // K2b: stable scatter.  Warp w of the CTA owns tile elements [w*256, (w+1)*256), visited in
@@ -204,10 +208,12 @@ __device__ __forceinline__ uint32_t peers_by_ballot(uint32_t dg, int bits, bool 
 // histogram.  Element order inside the tile is therefore preserved.  The tile is first reordered
 // by digit in shared memory and then written out in digit runs (coalesced stores).
 // vin == nullptr: values are the element indices (first pass; identity permutation).
+template <int BITS>
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift, int bits,
+    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift,
     const uint32_t* __restrict__ hist_scan, SegLayout sl) {
+  constexpr int bits = BITS;
   constexpr int kWarps = kSortThreads / 32;
   constexpr int kPerWarp = kSortTile / kWarps;
   __shared__ uint32_t wcnt[kWarps][1 << kMaxDigitBits];
@@ -247,7 +253,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   for (int j = 0; j < kSortItems; ++j) {
     const bool valid = wbase + j * 32 + lane < tile_n;
     const uint32_t dg = valid ? ((k[j] >> shift) & mask) : 0xffffffffu;
-    const uint32_t peers = peers_by_ballot(dg, bits, valid);
+    const uint32_t peers = peers_by_ballot<BITS>(dg, valid);
     const uint32_t cnt = valid ? wcnt[w][dg] : 0u;
     r[j] = cnt + __popc(peers & lt_mask);
     __syncwarp();
@@ -355,9 +361,28 @@ static cudaError_t exclusive_scan(bnfft_plan_s* p, const uint32_t* in, uint32_t*
   return cudaGetLastError();
 }
 
+typedef void (*ScatterFn)(const uint32_t*, const uint32_t*, uint32_t*, uint32_t*, int64_t, int,
+                          const uint32_t*, SegLayout);
+static ScatterFn scatter_for(int bits) {
+  switch (bits) {
+    case 1: return radix_scatter_kernel<1>;
+    case 2: return radix_scatter_kernel<2>;
+    case 3: return radix_scatter_kernel<3>;
+    case 4: return radix_scatter_kernel<4>;
+    case 5: return radix_scatter_kernel<5>;
+    case 6: return radix_scatter_kernel<6>;
+    case 7: return radix_scatter_kernel<7>;
+    default: return radix_scatter_kernel<8>;
+  }
+}
+
 cudaError_t sort_prepare() {
-  return cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              2 * kSortTile * (int)sizeof(uint32_t));
+  for (int b = 1; b <= kMaxDigitBits; ++b) {
+    cudaError_t e = cudaFuncSetAttribute(scatter_for(b), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         2 * kSortTile * (int)sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
@@ -376,9 +401,8 @@ cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
       p->launches++;
       cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
       if (e != cudaSuccess) return e;
-      radix_scatter_kernel<<<(unsigned)sl.ntiles, kSortThreads, 2 * kSortTile * sizeof(uint32_t),
-                             p->stream>>>(
-          kin, vin, kout, vout, n, shift, b, p->d_hist, sl);
+      scatter_for(b)<<<(unsigned)sl.ntiles, kSortThreads, 2 * kSortTile * sizeof(uint32_t), p->stream>>>(
+          kin, vin, kout, vout, n, shift, p->d_hist, sl);
       p->launches++;
       std::swap(kin, kout);
       if (!vin) {
