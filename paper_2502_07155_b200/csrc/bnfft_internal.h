@@ -105,7 +105,7 @@ struct bnfft_plan_s {
   // nodes
   int64_t n = 0, cap = 0;
   bool nodes_set = false;
-  double* d_xs = nullptr;        // nodes n x d: sorted (xs_user false) or user order (xs_user true)
+  double* d_xs = nullptr;        // node copy n x d: user order (xs_user) or sorted (last radix pass)
   bool xs_user = false;          // d <= 2 user-blocked plans keep nodes in user order
   bool offsets_valid = false;    // key offsets built (lazily for xs_user plans)
   uint32_t* d_perm = nullptr;    // sorted pos -> user index
@@ -155,7 +155,7 @@ void timer_end(bnfft_plan_s* p, int stage, cudaEvent_t ev);
 cudaError_t launch_psihat(bnfft_plan_s* p);
 cudaError_t launch_tapfit(bnfft_plan_s* p, int NC, double* d_coef, double* d_err);
 cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n);
-cudaError_t launch_sort(bnfft_plan_s* p, int64_t n);
+cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n);
 cudaError_t sort_prepare();
 cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n);
 cudaError_t launch_deconv(bnfft_plan_s* p, const void* fhat);

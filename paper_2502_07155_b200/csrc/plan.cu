@@ -460,10 +460,10 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
                            p->stream)) != cudaSuccess)
     return cuda_fail(e, "status copy");
   timer_begin(p, ST_SORT, &ev);
-  if ((e = launch_sort(p, n)) != cudaSuccess) return cuda_fail(e, "sort kernels");
+  if ((e = launch_sort(p, x, n)) != cudaSuccess) return cuda_fail(e, "sort kernels");
   timer_end(p, ST_SORT, ev);
   p->offsets_valid = false;
-  if (!p->xs_user || p->opts.d >= 2) {   // sorted node copy and/or key offsets (binned gather)
+  if (p->opts.d >= 2) {   // key offsets for the binned gather (d = 1 builds them on demand)
     timer_begin(p, ST_BUILD, &ev);
     if ((e = launch_build(p, x, n)) != cudaSuccess) return cuda_fail(e, "build kernel");
     timer_end(p, ST_BUILD, ev);

@@ -28,8 +28,8 @@ enum { BAD_NOT_FINITE = 1, BAD_RANGE = 2, BAD_BOX = 3 };
 __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams kp,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                             unsigned long long* __restrict__ bad, double* __restrict__ xcopy) {
-  // xcopy != nullptr: the plan keeps the nodes in user order (d <= 2, user-blocked sort); the
-  // gather then reads xcopy[perm[i]] inside an L2-resident user block.
+  // xcopy != nullptr: user-order node copy (d <= 2 user-blocked plans: the gather reads xcopy[perm[i]]
+  // inside an L2-resident user block; or no radix pass: the identity permutation).
   // vals (identity permutation) is only written when no radix pass will run; the first pass
   // generates v = index itself.
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -212,7 +212,10 @@ template <int BITS>
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift,
-    const uint32_t* __restrict__ hist_scan, SegLayout sl) {
+    const uint32_t* __restrict__ hist_scan, SegLayout sl, const double* __restrict__ xin,
+    double* __restrict__ xsout, int d) {
+  // last pass only (xsout != nullptr): also writes the sorted node copy xs[pos] = x[perm[pos]];
+  // the random reads of x stay inside one L2-resident user block for d <= 2.
   constexpr int bits = BITS;
   constexpr int kWarps = kSortThreads / 32;
   constexpr int kPerWarp = kSortTile / kWarps;
@@ -301,7 +304,10 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     uint32_t dg = (kk >> shift) & mask;
     uint32_t pos = gbase[dg] + (uint32_t)li - tstart[dg];
     kout[pos] = kk;
-    vout[pos] = sval[li];
+    const uint32_t vv = sval[li];
+    vout[pos] = vv;
+    if (xsout)
+      for (int t = 0; t < d; ++t) xsout[(int64_t)pos * d + t] = __ldg(&xin[(int64_t)vv * d + t]);
   }
 }
 
@@ -346,7 +352,7 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
   if (n > 0) {
     keys_kernel<<<grid_for(n, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0,
                                                          p->sort_passes ? nullptr : p->d_v0, p->d_bad,
-                                                         p->xs_user ? p->d_xs : nullptr);
+                                                         (p->xs_user || !p->sort_passes) ? p->d_xs : nullptr);
     p->launches++;
   }
   return cudaGetLastError();
@@ -362,7 +368,7 @@ static cudaError_t exclusive_scan(bnfft_plan_s* p, const uint32_t* in, uint32_t*
 }
 
 typedef void (*ScatterFn)(const uint32_t*, const uint32_t*, uint32_t*, uint32_t*, int64_t, int,
-                          const uint32_t*, SegLayout);
+                          const uint32_t*, SegLayout, const double*, double*, int);
 static ScatterFn scatter_for(int bits) {
   switch (bits) {
     case 1: return radix_scatter_kernel<1>;
@@ -385,7 +391,7 @@ cudaError_t sort_prepare() {
   return cudaSuccess;
 }
 
-cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
+cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n) {
   uint32_t *kin = p->d_k0, *vin = nullptr, *kout = p->d_k1, *vout = p->d_v1;
   if (n > 0 && p->sort_passes > 0) {
     SegLayout sl;
@@ -401,8 +407,10 @@ cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
       p->launches++;
       cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
       if (e != cudaSuccess) return e;
+      const bool last = pass == p->sort_passes - 1;
       scatter_for(b)<<<(unsigned)sl.ntiles, kSortThreads, 2 * kSortTile * sizeof(uint32_t), p->stream>>>(
-          kin, vin, kout, vout, n, shift, p->d_hist, sl);
+          kin, vin, kout, vout, n, shift, p->d_hist, sl, x, (last && !p->xs_user) ? p->d_xs : nullptr,
+          p->opts.d);
       p->launches++;
       std::swap(kin, kout);
       if (!vin) {
@@ -423,7 +431,7 @@ cudaError_t launch_sort(bnfft_plan_s* p, int64_t n) {
 
 cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n) {
   build_kernel<<<grid_for(n + 1, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys,
-                                                            p->xs_user ? nullptr : p->d_xs,
+                                                            nullptr,   // xs comes from the sort
                                                             p->d_bin_start, n, p->opts.d,
                                                             p->nbins, p->ub_log2, p->nkeys);
   p->launches++;
