@@ -79,7 +79,9 @@ __device__ __forceinline__ float sinpi_r(float u) { return sinpif(u); }
 __device__ __forceinline__ double phi_r(double tau, const WinParams& w) { return phi_tau_d(tau, w); }
 __device__ __forceinline__ float phi_r(float tau, const WinParams& w) { return phi_tau_f(tau, w); }
 __device__ __forceinline__ double sqrt_r(double v) { return sqrt(v); }
-__device__ __forceinline__ float sqrt_r(float v) { return sqrtf(v); }
+// complex64 edge factors: MUFU reciprocal square root times v (~2 ulp; taps need ~1e-7 absolute),
+// v >= 0 (v == 0 only for Kronecker nodes, which do not use the factor)
+__device__ __forceinline__ float sqrt_r(float v) { return v * rsqrtf(fmaxf(v, 1e-30f)); }
 template <typename R> __device__ __forceinline__ R pi_r();
 template <> __device__ __forceinline__ double pi_r<double>() { return 3.141592653589793; }
 template <> __device__ __forceinline__ float pi_r<float>() { return 3.14159265f; }
@@ -98,9 +100,7 @@ __device__ __forceinline__ DimState<R> dim_state(double u_d, const GatherParams<
   DimState<R> st;
   st.u = (R)u_d;
   st.x = (R)(2.0 * u_d - 1.0);
-  st.hit = -1;
-  if (st.u == R(0)) st.hit = m - 1;
-  else if (st.u == R(1)) st.hit = m;
+  st.hit = (st.u == R(0)) ? m - 1 : ((st.u == R(1)) ? m : -1);
   if (POLY) {
     st.s = 0;
     if (p.edge_sqrt) {
@@ -441,9 +441,10 @@ __device__ __forceinline__ bool node_cell(double xv, double Lf, int64_t L, int& 
   const double Lx = __dmul_rn(Lf, xv);
   const double fl = floor(Lx);
   u = Lx - fl;
-  int64_t cc = (int64_t)fl + L / 2;
-  if (cc > L - 1) { cc = L - 1; u = 1.0; }   // fl(L x) == L/2 (defensive)
-  c = (int)cc;
+  const int L32 = (int)L;                  // L < 2^31
+  int cc = __double2int_rz(fl) + (L32 >> 1);
+  u = (cc > L32 - 1) ? 1.0 : u;            // fl(L x) == L/2 (defensive)
+  c = min(cc, L32 - 1);
   return true;
 }
 
