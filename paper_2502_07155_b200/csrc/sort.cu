@@ -229,8 +229,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   const int ndig = 1 << bits;
   const uint32_t mask = ndig - 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kWarps * (1 << kMaxDigitBits); i += kSortThreads)
-    if ((i & ((1 << kMaxDigitBits) - 1)) < ndig) (&wcnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < kWarps * ndig; i += kSortThreads) wcnt[i >> BITS][i & (ndig - 1)] = 0;
   {
     const int64_t h0 = hist_index(sl, blockIdx.x, 0, ndig);
     const int64_t hs = hist_index(sl, blockIdx.x, 1, ndig) - h0;   // stride between digits
@@ -285,9 +284,11 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   }
   if (lane == 31) wsum[w] = x;
   __syncthreads();
-  uint32_t before = 0;
-  for (int ww = 0; ww < w; ++ww) before += wsum[ww];
-  if (dg0 < ndig) tstart[dg0] = before + x - tcount;
+  if (dg0 < ndig) {
+    uint32_t before = 0;
+    for (int ww = 0; ww < w; ++ww) before += wsum[ww];
+    tstart[dg0] = before + x - tcount;
+  }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
