@@ -49,13 +49,22 @@ __global__ void __launch_bounds__(256) psihat_kernel(const double* __restrict__ 
   const int64_t half = M / 2;                      // k = 0..half
   const int64_t nrun = (half + 1 + kRun - 1) / kRun;
   double fmax_loc = 0.0, rmin_loc = 1e300;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrun;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k0 = r * kRun;
+  // two lanes per run: lane parity h sums quadrature nodes j = h, h+2, ...; the pair combines with
+  // one shuffle (fixed order: even-lane partial + odd-lane partial)
+  const int h = threadIdx.x & 1;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  // the loop bound is warp-uniform (the pair shuffle needs all 32 lanes); lanes past nrun compute a
+  // dummy run and store nothing
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t wbase = (gtid >> 5) << 4;          // first run of this warp (16 runs per warp)
+  for (int64_t rw = wbase; rw < nrun; rw += nthreads >> 1) {
+    const int64_t r = rw + ((threadIdx.x & 31) >> 1);
+    const bool live = r < nrun;
+    const int64_t k0 = (live ? r : 0) * kRun;
     double acc[kRun];
 #pragma unroll
     for (int t = 0; t < kRun; ++t) acc[t] = 0.0;
-    for (int j = 0; j < kQuadN; ++j) {
+    for (int j = h; j < kQuadN; j += 2) {
       double zs, zc;
       sincospi(2.0 * double(k0) * tq[j] / double(L), &zs, &zc);
       const double ws = sn[j], wc = cs[j], gj = g[j];
@@ -68,6 +77,12 @@ __global__ void __launch_bounds__(256) psihat_kernel(const double* __restrict__ 
         zs = ns;
       }
     }
+#pragma unroll
+    for (int t = 0; t < kRun; ++t) {
+      const double other = __shfl_xor_sync(0xffffffffu, acc[t], 1);
+      acc[t] = h ? other + acc[t] : acc[t] + other;
+    }
+    if (h || !live) continue;
 #pragma unroll
     for (int t = 0; t < kRun; ++t) {
       const int64_t k = k0 + t;
@@ -84,10 +99,9 @@ __global__ void __launch_bounds__(256) psihat_kernel(const double* __restrict__ 
         psihat[half - k] = ph;
         q[half - k] = qq;
       }
-      if (k < half || k == half) {   // I_M contains -M/2 (= -half), not +M/2
-        fmax_loc = fmax(fmax_loc, fabs(double(L) * ph - 1.0));
-        rmin_loc = fmin(rmin_loc, fabs(ph) / fabs(p0));
-      }
+      // I_M contains -M/2 (= -half) but not +M/2; psi^(half) = psi^(-half) by evenness
+      fmax_loc = fmax(fmax_loc, fabs(double(L) * ph - 1.0));
+      rmin_loc = fmin(rmin_loc, fabs(ph) / fabs(p0));
     }
   }
   // block reduce, then one atomic per block
@@ -111,7 +125,7 @@ __global__ void __launch_bounds__(256) psihat_kernel(const double* __restrict__ 
 cudaError_t launch_psihat(bnfft_plan_s* p) {
   int64_t M = p->opts.M;
   int64_t nrun = (M / 2 + 1 + kRun - 1) / kRun;
-  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nrun + 255) / 256, 148 * 4));
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((2 * nrun + 255) / 256, 148 * 8));
   unsigned long long init[2] = {0ull, 0x7fefffffffffffffull};   // 0.0, DBL_MAX
   cudaError_t e = cudaMemcpyAsync(p->d_flat, init, sizeof(init), cudaMemcpyHostToDevice, p->stream);
   if (e != cudaSuccess) return e;
