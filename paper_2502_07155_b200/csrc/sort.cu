@@ -24,39 +24,75 @@ struct KeyParams {
 
 enum { BAD_NOT_FINITE = 1, BAD_RANGE = 2, BAD_BOX = 3 };
 
-// K1: validate + key.  bad = min over nodes of (index << 4 | code).
+// K1: validate + key.  bad = min over nodes of (index << 4 | code).  Each thread handles a pair of
+// consecutive nodes with 16-byte loads/stores (2*D doubles, 2 keys).
+template <int D>
+__device__ __forceinline__ uint32_t node_key(const double* xv, const KeyParams& kp, int& code) {
+  uint32_t key = 0;
+  bool nonfinite = false, range = false, box = false;
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    const double v = xv[t];
+    if (!isfinite(v)) { nonfinite = true; continue; }
+    if (!(v >= -0.5 && v < 0.5)) { range = true; continue; }
+    if (kp.strict && !(v >= kp.box_lo && v <= kp.box_hi)) box = true;
+    const double Lx = __dmul_rn(kp.Lf, v);
+    int c = __double2int_rz(floor(Lx)) + (int)(kp.L >> 1);
+    c = min(c, (int)kp.L - 1);         // fl(L x) == L/2 for x < 1/2 (defensive)
+    key = key * (uint32_t)kp.nb[t] + ((uint32_t)c >> kp.log2W[t]);
+  }
+  code = nonfinite ? BAD_NOT_FINITE : range ? BAD_RANGE : box ? BAD_BOX : 0;
+  return code ? 0u : key;
+}
+
+template <int D>
 __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams kp,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                            unsigned long long* __restrict__ bad, double* __restrict__ xcopy) {
+                            unsigned long long* __restrict__ bad, double* __restrict__ xcopy,
+                            int aligned16) {
   // xcopy != nullptr: user-order node copy (d <= 2 user-blocked plans: the gather reads xcopy[perm[i]]
   // inside an L2-resident user block; or no radix pass: the identity permutation).
   // vals (identity permutation) is only written when no radix pass will run; the first pass
-  // generates v = index itself.
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t key = 0;
-    int code = 0;
-    bool nonfinite = false, range = false, box = false;
-    for (int t = 0; t < kp.d; ++t) {
-      double xv = x[i * kp.d + t];
-      if (xcopy) xcopy[i * kp.d + t] = xv;
-      if (!isfinite(xv)) { nonfinite = true; continue; }
-      if (!(xv >= -0.5 && xv < 0.5)) { range = true; continue; }
-      if (kp.strict && !(xv >= kp.box_lo && xv <= kp.box_hi)) box = true;
-      double Lx = __dmul_rn(kp.Lf, xv);
-      int64_t c = (int64_t)floor(Lx) + kp.L / 2;
-      if (c > kp.L - 1) c = kp.L - 1;   // fl(L x) == L/2 for x < 1/2 (non-power-of-2 L only)
-      key = key * (uint32_t)kp.nb[t] + (uint32_t)(c >> kp.log2W[t]);
+  // generates v = index itself.  aligned16 == 0 (x not 16-byte aligned): scalar loads.
+  const int64_t npair = (n + 1) / 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npair;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 2 * q;
+    double xv[2 * D];
+    const bool full = i + 1 < n;
+    if (full && aligned16) {
+      const double2* src = reinterpret_cast<const double2*>(x + i * D);
+#pragma unroll
+      for (int h = 0; h < D; ++h) {
+        const double2 v = __ldg(&src[h]);
+        xv[2 * h] = v.x;
+        xv[2 * h + 1] = v.y;
+      }
+      if (xcopy) {
+        double2* dstc = reinterpret_cast<double2*>(xcopy + i * D);
+#pragma unroll
+        for (int h = 0; h < D; ++h) dstc[h] = make_double2(xv[2 * h], xv[2 * h + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 2 * D; ++t) {
+        const bool in = t < D || full;
+        xv[t] = in ? x[i * D + t] : 0.0;
+        if (xcopy && in) xcopy[i * D + t] = xv[t];
+      }
     }
-    if (nonfinite) code = BAD_NOT_FINITE;
-    else if (range) code = BAD_RANGE;
-    else if (box) code = BAD_BOX;
-    if (code) {
-      atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)code);
-      key = 0;
+    int c0 = 0, c1 = 0;
+    const uint32_t k0 = node_key<D>(xv, kp, c0);
+    const uint32_t k1 = full ? node_key<D>(xv + D, kp, c1) : 0u;
+    if (c0) atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)c0);
+    if (c1) atomicMin(bad, ((unsigned long long)(i + 1) << 4) | (unsigned long long)c1);
+    if (full) {
+      reinterpret_cast<uint2*>(keys)[q] = make_uint2(k0, k1);
+      if (vals) reinterpret_cast<uint2*>(vals)[q] = make_uint2((uint32_t)i, (uint32_t)(i + 1));
+    } else {
+      keys[i] = k0;
+      if (vals) vals[i] = (uint32_t)i;
     }
-    keys[i] = key;
-    if (vals) vals[i] = (uint32_t)i;
   }
 }
 
@@ -351,9 +387,11 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
   cudaError_t e = cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), p->stream);
   if (e != cudaSuccess) return e;
   if (n > 0) {
-    keys_kernel<<<grid_for(n, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0,
-                                                         p->sort_passes ? nullptr : p->d_v0, p->d_bad,
-                                                         (p->xs_user || !p->sort_passes) ? p->d_xs : nullptr);
+    auto kfn = p->opts.d == 1 ? keys_kernel<1> : p->opts.d == 2 ? keys_kernel<2> : keys_kernel<3>;
+    kfn<<<grid_for((n + 1) / 2, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0,
+                                                           p->sort_passes ? nullptr : p->d_v0, p->d_bad,
+                                                           (p->xs_user || !p->sort_passes) ? p->d_xs : nullptr,
+                                                           ((uintptr_t)x & 15) == 0 ? 1 : 0);
     p->launches++;
   }
   return cudaGetLastError();
