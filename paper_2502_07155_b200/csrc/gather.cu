@@ -132,7 +132,9 @@ cudaError_t gather_prepare(bnfft_plan_s* p) {
   if (!fn) return cudaErrorInvalidValue;
   if (p->opts.d == 1 && p->opts.batch == 1) {
     // two contiguous windows (double buffer) of 12 KB each; persistent grid sized by occupancy
-    p->gather_box_cap = (int)((12u << 10) / p->csize);
+    // window: chunk cells (~256*NPT at density 1) + one bin + halo, capped at 40 KB per buffer
+    p->gather_box_cap = (int)(std::min<size_t>(40u << 10, std::max<size_t>(12u << 10,
+                        ((size_t)2048 + ((size_t)1 << p->bin_log2[0])) * p->csize)) / p->csize);
     p->gather_smem = 2 * (size_t)p->gather_box_cap * p->csize;
     p->gather_bt = 1;
     p->gather_smax = 1;

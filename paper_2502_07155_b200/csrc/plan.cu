@@ -1,6 +1,7 @@
 // Host orchestration of the C ABI declared in include/bnfft.h: option validation (readings
 // A1, A2, A7), device buffers, cuFFT plan, stage sequencing and per-stage CUDA-event timing.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -277,6 +278,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
 
   // node binning geometry (row a1)
   int lg = 7;
+  if (const char* ev = getenv("BNFFT_D1_BIN_LOG2")) lg = atoi(ev);   // tuning knob (d = 1)
   if (o->d == 2) lg = 4;
   if (o->d == 3) lg = o->batch > 1 ? 2 : 3;
   int lgL = 0;
