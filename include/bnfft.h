@@ -70,7 +70,11 @@ typedef enum { BNFFT_C64 = 0, BNFFT_C128 = 1 } bnfft_prec;
 enum {
   BNFFT_STRICT_DOMAIN = 1u,  /* reject nodes outside the closed feasible box   */
   BNFFT_TIMING = 8u,         /* record per-stage CUDA events (read with bnfft_get_timing)     */
-  BNFFT_EXACT_TAPS = 16u     /* gather evaluates sinc * phi directly (no tap polynomials)       */
+  BNFFT_EXACT_TAPS = 16u,    /* gather evaluates sinc * phi directly (no tap polynomials)       */
+  BNFFT_ALG1 = 32u           /* classical NFFT, Algorithm 1: phi^ deconvolution,
+                                periodic short sums with the window phi (no sinc); nodes on the
+                                torus [-1/2,1/2)^d.  d = 1; sinh / cKB windows; default shape
+                                beta = 2 pi m (1 - 1/(2 sigma)) (reading A17)               */
 };
 
 /* Plan options.  d: 1..3.  M: even >= 2.  sigma >= 1, L = 2 ceil(ceil(sigma M)/2).
@@ -78,7 +82,7 @@ enum {
  * window: bnfft_window.  shape: beta (sinh, cKB) or s in x units (Gaussian); <= 0 selects the
  * default of readings A1/A2.  prec: arithmetic of steps 1-3 (C64: fp32 complex64 grid and
  * taps; C128: fp64).  Nodes are always float64.  batch >= 1 spectra share one node set.
- * flags: BNFFT_STRICT_DOMAIN | BNFFT_TIMING | BNFFT_EXACT_TAPS.  device: CUDA ordinal.  stream: cudaStream_t
+ * flags: BNFFT_STRICT_DOMAIN | BNFFT_TIMING | BNFFT_EXACT_TAPS | BNFFT_ALG1.  device: CUDA ordinal.  stream: cudaStream_t
  * (NULL = legacy default stream) on which every kernel and copy of this plan is issued. */
 typedef struct {
   int32_t d;

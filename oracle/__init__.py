@@ -7,3 +7,4 @@ section by section.  Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s
 this package shares no code with it.
 """
 from .bandlimited import *  # noqa: F401,F403
+from . import nfft  # noqa: F401  (Algorithm 1 and the §5 comparison)

@@ -25,6 +25,7 @@ constexpr int kQuadN = 64;            // Gauss-Legendre points for psi^ (reading
 // Window parameters in grid units tau = L x (|tau| <= m is the support).
 struct WinParams {
   int window;        // bnfft_window
+  int alg1;          // 1: classical NFFT (Algorithm 1): kernel phi instead of psi = sinc * phi
   int m;
   double inv_m;      // 1/m
   double beta;       // sinh / cKB shape

@@ -101,6 +101,7 @@ __device__ __forceinline__ DimState<R> dim_state(double u_d, const GatherParams<
   st.u = (R)u_d;
   st.x = (R)(2.0 * u_d - 1.0);
   st.hit = (st.u == R(0)) ? m - 1 : ((st.u == R(1)) ? m : -1);
+  if (p.wp.alg1) st.hit = -1;   // Algorithm 1: phi(l/L) is no Kronecker delta
   if (POLY) {
     st.s = 0;
     if (p.edge_sqrt) {
@@ -139,6 +140,7 @@ __device__ __forceinline__ R tap_weight(const DimState<R>& st, int i, const Gath
   } else {
     const int j = m - 1 - i;
     const R tau = st.u + (R)j;
+    if (p.wp.alg1) return phi_r(tau, p.wp);          // Algorithm 1: the window itself
     const R sg = (j & 1) ? -st.s : st.s;
     return sg / (pi_r<R>() * tau) * phi_r(tau, p.wp);
   }
@@ -495,14 +497,20 @@ __device__ __forceinline__ Window1 issue_window1(const GatherParams<R>& p, const
   win.staged = win.nbox <= p.boxcap;
   if (win.staged) {
     const int64_t g0 = lo > 0 ? lo : (int64_t)0, g1 = hi < p.L ? hi : p.L;
+    const bool periodic = p.wp.alg1 != 0;     // Algorithm 1: periodic index set (eq. indexset_x)
     if (threadIdx.x == 0) {
-      const uint32_t bytes = (uint32_t)((g1 - g0) * (int64_t)sizeof(C));
+      const int64_t wlo = periodic ? (g0 - lo) : 0, whi = periodic ? (hi - g1) : 0;
+      const uint32_t bytes = (uint32_t)((g1 - g0 + wlo + whi) * (int64_t)sizeof(C));
       mbar_expect_tx(bar, bytes);
-      if (bytes) tma_bulk_g2s(buf + (g0 - lo), (const C*)p.grid + g0, bytes, bar);
+      if (g1 > g0) tma_bulk_g2s(buf + (g0 - lo), (const C*)p.grid + g0, (uint32_t)((g1 - g0) * sizeof(C)), bar);
+      if (wlo) tma_bulk_g2s(buf, (const C*)p.grid + (lo + p.L), (uint32_t)(wlo * sizeof(C)), bar);
+      if (whi) tma_bulk_g2s(buf + (g1 - lo), (const C*)p.grid, (uint32_t)(whi * sizeof(C)), bar);
     }
-    // zero extension outside I_L (generic stores, disjoint from the TMA range)
-    for (int64_t q = threadIdx.x; q < g0 - lo; q += kGatherThreads) buf[q] = czero<C>();
-    for (int64_t q = (g1 - lo) + threadIdx.x; q < hi - lo; q += kGatherThreads) buf[q] = czero<C>();
+    if (!periodic) {
+      // zero extension outside I_L (generic stores, disjoint from the TMA range)
+      for (int64_t q = threadIdx.x; q < g0 - lo; q += kGatherThreads) buf[q] = czero<C>();
+      for (int64_t q = (g1 - lo) + threadIdx.x; q < hi - lo; q += kGatherThreads) buf[q] = czero<C>();
+    }
   }
   return win;
 }
@@ -569,7 +577,8 @@ __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_co
         const int64_t l0 = (int64_t)c - (m - 1);
 #pragma unroll
         for (int kk = 0; kk < T; ++kk) {
-          const int64_t pos = l0 + kk;
+          int64_t pos = l0 + kk;
+          if (p.wp.alg1) pos = pos < 0 ? pos + p.L : (pos >= p.L ? pos - p.L : pos);
           if (pos >= 0 && pos < p.L) cmac(acc, w[kk], __ldg(&grid[pos]));
         }
       }

@@ -224,7 +224,13 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   if (o->prec != BNFFT_C64 && o->prec != BNFFT_C128) { set_error("prec"); return BNFFT_E_INVALID_ARG; }
   if (o->batch < 1) { set_error("batch >= 1"); return BNFFT_E_INVALID_ARG; }
   if (!gather_supported(o->d, o->m)) { set_error("m outside the compiled range for this d"); return BNFFT_E_UNSUPPORTED; }
+  const bool alg1 = (o->flags & BNFFT_ALG1) != 0;
+  if (alg1 && (o->d != 1 || o->window == BNFFT_GAUSS || o->batch != 1)) {
+    set_error("BNFFT_ALG1 is compiled for d = 1, batch 1, sinh/cKB windows");
+    return BNFFT_E_UNSUPPORTED;
+  }
   double shape = o->shape;
+  if (!(shape > 0) && alg1) shape = 2.0 * M_PI * o->m * (1.0 - (double)o->M / (2.0 * (double)L));   // A17
   if (!(shape > 0)) {
     if (o->window == BNFFT_GAUSS) {
       if (L == o->M) { set_error("Gaussian default s needs L > M (reading A2)"); return BNFFT_E_BAD_WINDOW_PARAM; }
@@ -259,6 +265,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
 
   WinParams& w = p->wp;
   w.window = o->window;
+  w.alg1 = alg1 ? 1 : 0;
   w.m = o->m;
   w.inv_m = 1.0 / o->m;
   w.inv_m_f = (float)w.inv_m;

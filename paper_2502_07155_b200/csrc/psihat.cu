@@ -1,5 +1,6 @@
 // Algorithm 2 step 0(a): psi^_1(k), k in I_M, on the device, plus the
-// plan-time tap polynomials of the gather (row a6).
+// plan-time tap polynomials of the gather (row a6).  With BNFFT_ALG1 the same kernels compute
+// Algorithm 1's phi^_1(k) and fit the taps of the window phi (no sinc factor).
 //
 // psi^(v) = int psi(t) e^{-2 pi i v t} dt with psi even and supported on
 // [-m/L, m/L], so psi^(v) = 2 int_0^{m/L} psi(t) cos(2 pi v t) dt.  Reading A4:
@@ -31,7 +32,8 @@ __global__ void __launch_bounds__(256) psihat_kernel(const double* __restrict__ 
     double s, c;
     sincos(theta, &s, &c);
     double tau = wp.m * s;
-    double sinc = sinpi(tau) / (M_PI * tau);   // tau > 0 at interior GL nodes
+    // tau > 0 at interior GL nodes; Algorithm 1 transforms the window itself (phi^)
+    double sinc = wp.alg1 ? 1.0 : sinpi(tau) / (M_PI * tau);
     g[threadIdx.x] = w * (double(wp.m) / double(L)) * c * sinc * phi_tau_d(tau, wp);
     tq[threadIdx.x] = tau;
     double ss, cc;
@@ -140,7 +142,7 @@ cudaError_t launch_psihat(bnfft_plan_s* p) {
 __device__ double tap_exact_d(int i, double u, int m, const WinParams& wp, bool edge_sqrt,
                               bool divide_edge) {
   const double tau = u + double(m - 1 - i);
-  const double sinc = (tau == 0.0) ? 1.0 : sinpi(tau) / (M_PI * tau);
+  const double sinc = (tau == 0.0 || wp.alg1) ? 1.0 : sinpi(tau) / (M_PI * tau);
   double v = sinc * phi_tau_d(tau, wp);
   if (edge_sqrt && divide_edge && (i == 0 || i == 2 * m - 1)) {
     // sinh edge taps: v = sinc * sinh(beta r)/sinh(beta) with r = sqrt(1-(tau/m)^2);
