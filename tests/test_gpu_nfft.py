@@ -4,7 +4,7 @@ import pytest
 
 import oracle as O
 import synth
-from oracle import nfft as N
+from oracle import nfft as NF
 
 pytestmark = pytest.mark.gpu
 TOL = {"c128": 1e-12, "c64": 1e-5}
@@ -27,7 +27,7 @@ def test_alg1_parity(prec, window, M, m, N):
     plan = bnfft.Plan(1, M, 2.0, m, window, prec, alg1=True)
     plan.set_nodes(torch.from_numpy(x).cuda())
     f = plan.execute(torch.from_numpy(fh).cuda()).cpu().numpy()
-    ref = N.algorithm1(x, fh.astype(np.complex128), M, 2.0, m, window)
+    ref = NF.algorithm1(x, fh.astype(np.complex128), M, 2.0, m, window)
     assert abs(plan.info().shape - ref["shape"]) < 1e-12 * ref["shape"]
     assert np.max(np.abs(plan.psihat() - ref["phihat"]) / np.abs(ref["phihat"])) < 2e-13
     assert rel_l2(f, ref["f"]) <= TOL[prec]
