@@ -160,6 +160,19 @@ BNFFT_API int bnfft_set_nodes(struct bnfft_plan_s* plan, int64_t n, const double
  * asynchronous; errors of earlier asynchronous work surface as BNFFT_E_CUDA. */
 BNFFT_API int bnfft_execute(struct bnfft_plan_s* plan, const void* fhat_dev, void* f_dev);
 
+/* Step 3 alone with caller-provided grid samples: f_j = sum_{l in I_L} s_l psi(x_j - l/L), i.e. the
+ * regularized Shannon sampling formula with localized sampling (eq. Rmf(x)_multi) restricted
+ * to l in I_L (first equality of P:463); with BNFFT_ALG1 the periodic sum with the window,
+ * f~_j = sum_{l in I_{L,m}(x_j)} s_l phi~_m(x_j - l/L) (the matrix B of P:184-199).  samples_dev:
+ * device, batch x L^d complex (plan precision), centred (l_t + L/2), row-major.  f_dev as in
+ * bnfft_execute.  Stream-ordered; requires set_nodes. */
+BNFFT_API int bnfft_interpolate(struct bnfft_plan_s* plan, const void* samples_dev, void* f_dev);
+
+/* The kernel's Fourier transform at arbitrary real frequencies (the quadrature of step 0(a)):
+ * psi^_1(v) = 2 int_0^{m/L} psi(t) cos(2 pi v t) dt, or phi^_1(v) with BNFFT_ALG1.  n values
+ * from host v_host into host out_host (computed on the device; synchronous). */
+BNFFT_API int bnfft_kernel_hat(struct bnfft_plan_s* plan, int64_t n, const double* v_host, double* out_host);
+
 /* End-to-end helper with HOST buffers: copies x (n x d float64) and f^ host->device, runs
  * set_nodes and execute, copies f device->host, and synchronizes.  Pinned host memory gives
  * asynchronous DMA; pageable memory works but is staged by the CUDA driver. */

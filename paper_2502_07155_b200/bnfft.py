@@ -70,6 +70,8 @@ _sig = {
     "bnfft_set_nodes": (c_int, [_P, c_int64, c_void_p, POINTER(c_int64)]),
     "bnfft_execute": (c_int, [_P, c_void_p, c_void_p]),
     "bnfft_transform_host": (c_int, [_P, c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_int64)]),
+    "bnfft_interpolate": (c_int, [_P, c_void_p, c_void_p]),
+    "bnfft_kernel_hat": (c_int, [_P, c_int64, c_void_p, c_void_p]),
     "bnfft_get_info": (c_int, [_P, POINTER(bnfft_info)]),
     "bnfft_get_timing": (c_int, [_P, POINTER(bnfft_timing)]),
     "bnfft_reset_timing": (c_int, [_P]),
@@ -153,6 +155,22 @@ class Plan:
         if out is None:
             out = t.empty((self.batch, self.n), dtype=self.cdtype, device=fhat.device)
         check(bnfft_execute(self.h, _ptr(fhat), _ptr(out) if self.n else None), "bnfft_execute")
+        return out
+
+    def interpolate(self, samples, out=None):
+        """Step 3 alone from grid samples (batch x L^d, centred): regularized Shannon formula."""
+        t = self._torch
+        assert samples.dtype == self.cdtype and samples.is_cuda and samples.is_contiguous()
+        if out is None:
+            out = t.empty((self.batch, self.n), dtype=self.cdtype, device=samples.device)
+        check(bnfft_interpolate(self.h, _ptr(samples), _ptr(out) if self.n else None), "bnfft_interpolate")
+        return out
+
+    def kernel_hat(self, v):
+        import numpy as np
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty_like(v)
+        check(bnfft_kernel_hat(self.h, v.size, v.ctypes.data, out.ctypes.data), "bnfft_kernel_hat")
         return out
 
     def transform_host(self, x_host, fhat_host, f_host) -> None:

@@ -155,6 +155,7 @@ void timer_end(bnfft_plan_s* p, int stage, cudaEvent_t ev);
 // launchers
 cudaError_t launch_psihat(bnfft_plan_s* p);
 cudaError_t launch_tapfit(bnfft_plan_s* p, int NC, double* d_coef, double* d_err);
+cudaError_t launch_kernel_hat(bnfft_plan_s* p, const double* v_dev, double* out_dev, int64_t n);
 cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n);
 cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n);
 cudaError_t sort_prepare();

@@ -527,6 +527,36 @@ int bnfft_execute(bnfft_plan_s* p, const void* fhat, void* f) {
   return BNFFT_OK;
 }
 
+int bnfft_interpolate(bnfft_plan_s* p, const void* samples, void* f) {
+  if (!p) return BNFFT_E_INVALID_ARG;
+  if (!p->nodes_set) { set_error("call bnfft_set_nodes first"); return BNFFT_E_NODES_NOT_SET; }
+  if (!samples || (p->n > 0 && !f)) { set_error("NULL buffer"); return BNFFT_E_INVALID_ARG; }
+  cudaSetDevice(p->device);
+  cudaError_t e = cudaMemcpyAsync(p->d_grid, samples, (size_t)p->Ld * p->opts.batch * p->csize,
+                                  cudaMemcpyDeviceToDevice, p->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "copy samples");
+  cudaEvent_t ev;
+  timer_begin(p, ST_GATHER, &ev);
+  if ((e = launch_gather(p, f)) != cudaSuccess) return cuda_fail(e, "gather kernel");
+  timer_end(p, ST_GATHER, ev);
+  return BNFFT_OK;
+}
+
+int bnfft_kernel_hat(bnfft_plan_s* p, int64_t n, const double* v_host, double* out_host) {
+  if (!p || n < 0 || (n > 0 && (!v_host || !out_host))) return BNFFT_E_INVALID_ARG;
+  if (n == 0) return BNFFT_OK;
+  cudaSetDevice(p->device);
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc((void**)&d, 2 * n * sizeof(double));
+  if (e != cudaSuccess) return cuda_fail(e, "alloc kernel_hat");
+  e = cudaMemcpyAsync(d, v_host, n * sizeof(double), cudaMemcpyHostToDevice, p->stream);
+  if (e == cudaSuccess) e = launch_kernel_hat(p, d, d + n, n);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_host, d + n, n * sizeof(double), cudaMemcpyDeviceToHost, p->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  cudaFree(d);
+  return e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "kernel_hat");
+}
+
 int bnfft_transform_host(bnfft_plan_s* p, int64_t n, const double* x_host, const void* fhat_host,
                          void* f_host, int64_t* first_bad) {
   if (first_bad) *first_bad = -1;

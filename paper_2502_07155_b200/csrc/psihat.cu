@@ -137,6 +137,36 @@ cudaError_t launch_psihat(bnfft_plan_s* p) {
   return cudaGetLastError();
 }
 
+// psi^_1 (phi^_1 for Algorithm 1) at arbitrary frequencies v[i] (bnfft_kernel_hat).
+__global__ void kernel_hat_kernel(const double* __restrict__ gl, const double* __restrict__ v,
+                                  double* __restrict__ out, int64_t n, int64_t L, WinParams wp) {
+  __shared__ double g[kQuadN], tq[kQuadN];
+  if (threadIdx.x < kQuadN) {
+    double theta = gl[threadIdx.x];
+    double w = gl[kQuadN + threadIdx.x];
+    double s, c;
+    sincos(theta, &s, &c);
+    double tau = wp.m * s;
+    double sinc = wp.alg1 ? 1.0 : sinpi(tau) / (M_PI * tau);
+    g[threadIdx.x] = w * (double(wp.m) / double(L)) * c * sinc * phi_tau_d(tau, wp);
+    tq[threadIdx.x] = tau;
+  }
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < kQuadN; ++j) acc += g[j] * cospi(2.0 * v[i] * tq[j] / double(L));
+    out[i] = 2.0 * acc;
+  }
+}
+
+cudaError_t launch_kernel_hat(bnfft_plan_s* p, const double* v_dev, double* out_dev, int64_t n) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  kernel_hat_kernel<<<blocks, 256, 0, p->stream>>>(p->d_gl, v_dev, out_dev, n, p->L, p->wp);
+  p->launches++;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ tap polynomials (plan time)
 // Exact tap value w_i(u) = psi(u + m-1-i) (grid units) divided by the sinh edge factor.
 __device__ double tap_exact_d(int i, double u, int m, const WinParams& wp, bool edge_sqrt,
