@@ -26,6 +26,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def beta_a1(M, L, m):
+    """Reading A1 (Algorithm 2's default sinh beta), also used for the NFFT in the 'same-beta' runs."""
+    return math.pi * m * (1.0 - M / L)
+
+
 def fig1(bn, torch, P=100_000, S=32, M=20, m=5, sigma=2.0, window="sinh"):
     L = 2 * math.ceil(math.ceil(sigma * M) / 2)
     xp = -0.5 + np.arange(P) / P
@@ -37,8 +42,9 @@ def fig1(bn, torch, P=100_000, S=32, M=20, m=5, sigma=2.0, window="sinh"):
         x = xp if dom == "full" else xp[(xp >= -0.5 + m / L) & (xp < 0.5 - m / L)]
         xd = torch.from_numpy(np.ascontiguousarray(x[:, None])).cuda()
         e = np.exp(2j * np.pi * np.multiply.outer(v, x))            # (nv, P)
-        for name, alg1, use_hat in (("nfft", True, True), ("alg2", False, True), ("alg2_nohat", False, False)):
-            plan = bn.Plan(1, M, sigma, m, window, "c128", alg1=alg1)
+        for name, alg1, use_hat, shape in (("nfft", True, True, 0.0), ("nfft_samebeta", True, True, beta_a1(M, L, m)),
+                                           ("alg2", False, True, 0.0), ("alg2_nohat", False, False, 0.0)):
+            plan = bn.Plan(1, M, sigma, m, window, "c128", alg1=alg1, shape=shape)
             plan.set_nodes(xd)
             hat = plan.kernel_hat(v) if use_hat else np.full(len(v), 1.0 / L)
             errs = np.empty(len(v))
@@ -52,7 +58,7 @@ def fig1(bn, torch, P=100_000, S=32, M=20, m=5, sigma=2.0, window="sinh"):
 
 
 def fig2(bn, torch, Ms=tuple(range(20, 1001, 20)), m=5, sigma=2.0, window="sinh"):
-    out = {"M": list(Ms), "m": m, "window": window, "alg2": [], "nfft": []}
+    out = {"M": list(Ms), "m": m, "window": window, "alg2": [], "nfft": [], "nfft_samebeta": []}
     for M in Ms:
         L = 2 * math.ceil(math.ceil(sigma * M) / 2)
         N = M // 2
@@ -62,8 +68,8 @@ def fig2(bn, torch, Ms=tuple(range(20, 1001, 20)), m=5, sigma=2.0, window="sinh"
         fh = ((2.0 / M) * np.clip(1.0 - np.abs(2.0 * k / M), 0.0, None)).astype(np.complex128)[None]
         exact = np.sinc(M * x / 2) ** 2                      # numpy sinc(y) = sin(pi y)/(pi y)
         xd = torch.from_numpy(np.ascontiguousarray(x[:, None])).cuda()
-        for name, alg1 in (("alg2", False), ("nfft", True)):
-            plan = bn.Plan(1, M, sigma, m, window, "c128", alg1=alg1)
+        for name, alg1, shape in (("alg2", False, 0.0), ("nfft", True, 0.0), ("nfft_samebeta", True, beta_a1(M, L, m))):
+            plan = bn.Plan(1, M, sigma, m, window, "c128", alg1=alg1, shape=shape)
             plan.set_nodes(xd)
             f = plan.execute(torch.from_numpy(fh).cuda())[0].cpu().numpy()
             out[name].append(float(np.max(np.abs(f - exact))))
@@ -86,10 +92,11 @@ def main():
     inner = np.abs(v) <= r1["M"] / 2 - r1["m"] / r1["L"]
     summary = {
         "fig1_max_err_truncated_inband": {k: float(np.max(np.array(r1[f"{k}_truncated"])[inner]))
-                                          for k in ("nfft", "alg2", "alg2_nohat")},
+                                          for k in ("nfft", "nfft_samebeta", "alg2", "alg2_nohat")},
         "fig1_max_err_full_inband": {k: float(np.max(np.array(r1[f"{k}_full"])[inner]))
-                                     for k in ("nfft", "alg2", "alg2_nohat")},
+                                     for k in ("nfft", "nfft_samebeta", "alg2", "alg2_nohat")},
         "fig2_M>80_alg2_better_fraction": float(np.mean([a2 < nf for M, a2, nf in zip(r2["M"], r2["alg2"], r2["nfft"]) if M > 80])),
+        "fig2_M>80_alg2_better_fraction_samebeta": float(np.mean([a2 < nf for M, a2, nf in zip(r2["M"], r2["alg2"], r2["nfft_samebeta"]) if M > 80])),
         "seconds": time.time() - t0,
     }
     json.dump({"fig1": r1, "fig2": r2, "summary": summary}, open(a.out, "w"))
