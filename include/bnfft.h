@@ -74,7 +74,11 @@ enum {
   BNFFT_ALG1 = 32u           /* classical NFFT, Algorithm 1: phi^ deconvolution,
                                 periodic short sums with the window phi (no sinc); nodes on the
                                 torus [-1/2,1/2)^d.  d = 1; sinh / cKB windows; default shape
-                                beta = 2 pi m (1 - 1/(2 sigma)) (reading A17)               */
+                                beta = 2 pi m (1 - 1/(2 sigma)) (reading A17)               */,
+  BNFFT_PRECOMPUTE_PSI = 64u /* Algorithm 2 step 0(b): set_nodes evaluates the kernel at every
+                                (node, tap) once and stores it (2m values per node); execute reads
+                                them instead of evaluating the tap polynomials.  d = 1, batch 1.
+                                Costs 2m * (4|8) bytes per node of device memory.              */
 };
 
 /* Plan options.  d: 1..3.  M: even >= 2.  sigma >= 1, L = 2 ceil(ceil(sigma M)/2).
@@ -82,7 +86,7 @@ enum {
  * window: bnfft_window.  shape: beta (sinh, cKB) or s in x units (Gaussian); <= 0 selects the
  * default of readings A1/A2.  prec: arithmetic of steps 1-3 (C64: fp32 complex64 grid and
  * taps; C128: fp64).  Nodes are always float64.  batch >= 1 spectra share one node set.
- * flags: BNFFT_STRICT_DOMAIN | BNFFT_TIMING | BNFFT_EXACT_TAPS | BNFFT_ALG1.  device: CUDA ordinal.  stream: cudaStream_t
+ * flags: BNFFT_STRICT_DOMAIN | BNFFT_TIMING | BNFFT_EXACT_TAPS | BNFFT_ALG1 | BNFFT_PRECOMPUTE_PSI.  device: CUDA ordinal.  stream: cudaStream_t
  * (NULL = legacy default stream) on which every kernel and copy of this plan is issued. */
 typedef struct {
   int32_t d;

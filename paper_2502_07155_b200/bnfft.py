@@ -37,6 +37,7 @@ BNFFT_STRICT_DOMAIN = 1
 BNFFT_TIMING = 8
 BNFFT_EXACT_TAPS = 16
 BNFFT_ALG1 = 32
+BNFFT_PRECOMPUTE_PSI = 64
 WINDOWS = {"sinh": BNFFT_SINH, "gauss": BNFFT_GAUSS, "ckb": BNFFT_CKB}
 PRECS = {"c64": BNFFT_C64, "c128": BNFFT_C128}
 
@@ -114,7 +115,7 @@ class Plan:
     def __init__(self, d: int, M: int, sigma: float, m: int, window: str = "sinh",
                  prec: str = "c128", batch: int = 1, shape: float = 0.0, strict: bool = False,
                  timing: bool = False, exact_taps: bool = False, alg1: bool = False,
-                 device: int = 0, stream: int | None = None):
+                 precompute_psi: bool = False, device: int = 0, stream: int | None = None):
         import torch
         self._torch = torch
         if stream is None:
@@ -123,7 +124,8 @@ class Plan:
         o = bnfft_opts(d=d, M=M, sigma=sigma, m=m, window=WINDOWS[window], shape=shape,
                        prec=PRECS[prec], batch=batch,
                        flags=(BNFFT_STRICT_DOMAIN if strict else 0) | (BNFFT_TIMING if timing else 0)
-                       | (BNFFT_EXACT_TAPS if exact_taps else 0) | (BNFFT_ALG1 if alg1 else 0),
+                       | (BNFFT_EXACT_TAPS if exact_taps else 0) | (BNFFT_ALG1 if alg1 else 0)
+                       | (BNFFT_PRECOMPUTE_PSI if precompute_psi else 0),
                        device=device, stream=stream)
         h = c_void_p()
         check(bnfft_plan_create(ctypes.byref(o), ctypes.byref(h)), "bnfft_plan_create")

@@ -130,6 +130,8 @@ struct bnfft_plan_s {
   int64_t gather_grid1 = 0;   // persistent grid size (SMs x resident CTAs)
   int gather_nslice = 1, gather_box_elems = 0, gather_bufstride = 0;
   int gather_tbox[3] = {1, 1, 1};
+  void* d_pre_w = nullptr;        // BNFFT_PRECOMPUTE_PSI: [n][2m] weights of the sorted nodes
+  int64_t pre_cap = 0;
   alignas(64) CUtensorMap tmap;   // d >= 2: TMA descriptor of the theta grid (host copy)
   CUtensorMap* d_tmap = nullptr;  // device (global memory) copy used by the kernel
   size_t gather_smem = 0;
@@ -165,6 +167,7 @@ cudaError_t launch_gather(bnfft_plan_s* p, void* out);
 int gather_supported(int d, int m);
 size_t gather_box_elems(const bnfft_plan_s* p);
 cudaError_t gather_prepare(bnfft_plan_s* p);
+cudaError_t launch_prepsi(bnfft_plan_s* p);
 int tap_coef_count(bool c128);
 
 }  // namespace bnfft

@@ -162,7 +162,7 @@ cudaError_t gather_prepare(bnfft_plan_s* p) {
 }
 
 template <typename R>
-static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
+static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, bool prepsi = false) {
   static_assert(sizeof(GatherParams<R>) < 32000, "kernel parameter limit");
   GatherParams<R> gp;
   memset(&gp, 0, sizeof(gp));
@@ -188,6 +188,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
   gp.wp = p->wp;
   gp.boxcap = p->gather_box_cap;
   gp.xs_user = p->xs_user ? 1 : 0;
+  gp.pre_w = (R*)p->d_pre_w;
   constexpr int NC = PolyN<R>::NC;
   constexpr int NH = PolyH<R>::NH;
   static_assert(2 * NH == NC, "even/odd split of the tap polynomials");
@@ -199,6 +200,12 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn) {
       }
   }
   void* args[] = {&gp};
+  if (prepsi) {   // grid-stride elementwise kernel, no shared memory
+    unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p->n + kGatherThreads - 1) / kGatherThreads, 148 * 16));
+    cudaError_t e3 = cudaLaunchKernel(fn, dim3(nb), dim3(kGatherThreads), args, 0, p->stream);
+    p->launches++;
+    return e3;
+  }
   gp.key_start = p->d_bin_start;
   gp.nkeys = p->nkeys;
   gp.nslice = p->gather_nslice;
@@ -237,6 +244,14 @@ cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
   const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1);
   if (!fn) return cudaErrorInvalidValue;
   return p->c128 ? launch_gather_t<double>(p, out, fn) : launch_gather_t<float>(p, out, fn);
+}
+
+// Algorithm 2 step 0(b): per-node tap weights for BNFFT_PRECOMPUTE_PSI (d = 1)
+cudaError_t launch_prepsi(bnfft_plan_s* p) {
+  if (p->n == 0) return cudaSuccess;
+  const void* fn = p->c128 ? gather_kernel_1d(p->opts.m + 200, p->tap_poly) : gather_kernel_1f(p->opts.m + 200, p->tap_poly);
+  if (!fn) return cudaErrorInvalidValue;
+  return p->c128 ? launch_gather_t<double>(p, nullptr, fn, true) : launch_gather_t<float>(p, nullptr, fn, true);
 }
 
 int tap_coef_count(bool c128) { return c128 ? PolyN<double>::NC : PolyN<float>::NC; }

@@ -63,6 +63,7 @@ struct GatherParams {
   R inv_m;
   int boxcap;             // d = 1 kernel: staged-box capacity in complex elements
   int xs_user;            // xs in user order: node i of the sorted order is xs[perm[i]]
+  R* pre_w;               // BNFFT_PRECOMPUTE_PSI: tap weights [n][2m] of the sorted nodes (or null)
   const uint32_t* key_start;   // binned kernel: first sorted position of each (user block, bin)
   int64_t nkeys;
   int tbox[3];            // binned kernel: TMA box extents per dim (dim 0 slowest), innermost padded
@@ -515,6 +516,13 @@ __device__ __forceinline__ Window1 issue_window1(const GatherParams<R>& p, const
   return win;
 }
 
+// row stride of the precomputed weight table: 2m rounded up to 16 bytes (vector loads)
+template <int T, typename R>
+struct PreStride {
+  static constexpr int V = 16 / (int)sizeof(R);
+  static constexpr int v = (T + V - 1) / V * V;
+};
+
 template <int T, typename R, bool POLY>
 __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_constant__ GatherParams<R> p) {
   using C = typename CT<R>::C;
@@ -565,9 +573,25 @@ __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_co
       int c;
       double u;
       if (!node_cell(cur.x[j], p.Lf, p.L, c, u)) continue;
-      const DimState<R> st = dim_state<T, R, POLY>(u, p);
       R w[T];
-      all_taps<T, POLY>(st, p, w);
+      if (p.pre_w) {   // Algorithm 2 step 0(b): weights precomputed by set_nodes
+        const int64_t i = k * (int64_t)kGatherThreads * NPT + j * kGatherThreads + threadIdx.x;
+        const R* src = p.pre_w + i * PreStride<T, R>::v;
+#pragma unroll
+        for (int q = 0; q < T; q += 16 / (int)sizeof(R)) {
+          if constexpr (sizeof(R) == 4) {
+            const float4 v4 = __ldg(reinterpret_cast<const float4*>(src + q));
+            w[q] = v4.x; w[q + 1] = v4.y;
+            if (q + 2 < T) { w[q + 2] = v4.z; w[q + 3] = v4.w; }
+          } else {
+            const double2 v2 = __ldg(reinterpret_cast<const double2*>(src + q));
+            w[q] = v2.x; w[q + 1] = v2.y;
+          }
+        }
+      } else {
+        const DimState<R> st = dim_state<T, R, POLY>(u, p);
+        all_taps<T, POLY>(st, p, w);
+      }
       C acc = czero<C>();
       if (wcur.staged) {
         const C* row = bcur + (c - (m - 1) - wcur.lo);
@@ -920,6 +944,24 @@ __global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_c
   }
 }
 
+// Algorithm 2 step 0(b), d = 1: the 2m weights psi(x_j - l/L) of every sorted node, stored
+// [n][2m] for the gather (BNFFT_PRECOMPUTE_PSI).
+template <int T, typename R, bool POLY>
+__global__ void __launch_bounds__(kGatherThreads) prepsi1_kernel(const __grid_constant__ GatherParams<R> p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t dst = __ldg(&p.perm[i]);
+    int c = 0;
+    double u = 0.0;
+    node_cell(__ldg(&p.xs[p.xs_user ? (int64_t)dst : i]), p.Lf, p.L, c, u);
+    const DimState<R> st = dim_state<T, R, POLY>(u, p);
+    R w[T];
+    all_taps<T, POLY>(st, p, w);
+    R* o = p.pre_w + i * PreStride<T, R>::v;
+#pragma unroll
+    for (int k = 0; k < T; ++k) o[k] = w[k];
+  }
+}
+
 template <int D, typename R, bool POLY, int MM>
 static const void* kernel_for(int m) {
   if (m == MM) {
@@ -928,6 +970,7 @@ static const void* kernel_for(int m) {
   }
   if constexpr (D == 1) {
     if (m == MM + 100) return (const void*)gather_kernel<1, 2 * MM, R, POLY>;
+    if (m == MM + 200) return (const void*)prepsi1_kernel<2 * MM, R, POLY>;
   }
   if constexpr (MM > 1) return kernel_for<D, R, POLY, MM - 1>(m);
   return nullptr;

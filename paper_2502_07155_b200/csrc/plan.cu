@@ -18,6 +18,7 @@ void set_error(const std::string& s) { g_err = s; }
 
 int cuda_fail(cudaError_t e, const char* what) {
   g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  (void)cudaGetLastError();   // a failed launch must not be reported again by a later check
   if (e == cudaErrorMemoryAllocation) return BNFFT_E_OOM;
   return BNFFT_E_CUDA;
 }
@@ -184,6 +185,7 @@ int bnfft_destroy(bnfft_plan_s* p) {
   dfree(p->d_fhat_stage);
   dfree(p->d_f_stage);
   dfree(p->d_tmap);
+  dfree(p->d_pre_w);
   free_nodes(p);
   if (p->h_bad) cudaFreeHost(p->h_bad);
   for (auto& t : p->pending) {
@@ -225,6 +227,10 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   if (o->batch < 1) { set_error("batch >= 1"); return BNFFT_E_INVALID_ARG; }
   if (!gather_supported(o->d, o->m)) { set_error("m outside the compiled range for this d"); return BNFFT_E_UNSUPPORTED; }
   const bool alg1 = (o->flags & BNFFT_ALG1) != 0;
+  if ((o->flags & BNFFT_PRECOMPUTE_PSI) && (o->d != 1 || o->batch != 1)) {
+    set_error("BNFFT_PRECOMPUTE_PSI is compiled for d = 1, batch 1");
+    return BNFFT_E_UNSUPPORTED;
+  }
   if (alg1 && (o->d != 1 || o->window == BNFFT_GAUSS || o->batch != 1)) {
     set_error("BNFFT_ALG1 is compiled for d = 1, batch 1, sinh/cKB windows");
     return BNFFT_E_UNSUPPORTED;
@@ -471,6 +477,22 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
   timer_begin(p, ST_SORT, &ev);
   if ((e = launch_sort(p, x, n)) != cudaSuccess) return cuda_fail(e, "sort kernels");
   timer_end(p, ST_SORT, ev);
+  if (p->opts.flags & BNFFT_PRECOMPUTE_PSI) {   // Algorithm 2 step 0(b)
+    const size_t wb = (size_t)std::max<int64_t>(n, 1) * ((2 * p->opts.m + 3) / 4 * 4) * (p->csize / 2);   // rows padded to 16 B
+    if (n > p->pre_cap) {
+      dfree(p->d_pre_w);
+      p->d_pre_w = nullptr;
+      if ((e = dmalloc(p, &p->d_pre_w, wb)) != cudaSuccess) return cuda_fail(e, "alloc psi table");
+      p->pre_cap = std::max<int64_t>(n, 1);
+    }
+    const int64_t n_prev = p->n;
+    p->n = n;   // the precompute kernel iterates over the new node set
+    timer_begin(p, ST_BUILD, &ev);
+    e = launch_prepsi(p);
+    p->n = n_prev;
+    if (e != cudaSuccess) return cuda_fail(e, "psi precompute");
+    timer_end(p, ST_BUILD, ev);
+  }
   p->offsets_valid = false;
   if (p->opts.d >= 2) {   // key offsets for the binned gather (d = 1 builds them on demand)
     timer_begin(p, ST_BUILD, &ev);

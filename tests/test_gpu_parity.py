@@ -317,3 +317,37 @@ def test_shards_bitwise(bn, torch, cid, d, M, N, prec):
         p.close()
     assert torch.equal(torch.cat(parts, dim=1), ref)
     full.close()
+
+
+# ----------------------------------------------------------------------------- step 0(b): PRECOMPUTE_PSI
+@pytest.mark.parametrize("prec,m,window,exact", [("c64", 4, "sinh", False), ("c128", 5, "sinh", False),
+                                                 ("c64", 3, "gauss", False), ("c64", 7, "ckb", True),
+                                                 ("c128", 2, "sinh", False)])
+def test_precompute_psi(bn, torch, prec, m, window, exact):
+    """BNFFT_PRECOMPUTE_PSI (Algorithm 2 step 0(b)): the stored per-node weights are the same
+    numbers the gather evaluates on the fly, so the result equals the default path bitwise and meets
+    parity with the oracle; odd m exercises the 16-byte row padding."""
+    cfg = synth.CONFIGS[2].scaled(M=1 << 11, m=m, N=70_001)
+    x = synth.make_nodes(cfg, variant=11)
+    fh = synth.make_spectrum(cfg, variant=11, prec=prec)
+    ref = oracle_f(x, fh, cfg.M, 2.0, m, window)["f"]
+    f0, p0 = run_gpu(bn, torch, x, fh, 1, cfg.M, 2.0, m, window, prec, exact_taps=exact)
+    f1, p1 = run_gpu(bn, torch, x, fh, 1, cfg.M, 2.0, m, window, prec, exact_taps=exact, precompute_psi=True)
+    assert np.array_equal(f0, f1)
+    assert rel_l2(f1, ref) <= TOL[prec]
+    # new nodes (fewer, then more) recompute the table
+    for n, v in ((5_003, 12), (90_001, 13)):
+        xn = synth.make_nodes(cfg, N=n, variant=v)
+        p1.set_nodes(torch.from_numpy(xn).cuda())
+        ft = torch.from_numpy(fh.astype(np.complex128 if prec == "c128" else np.complex64)).cuda()
+        fn = p1.execute(ft).cpu().numpy()
+        assert rel_l2(fn, oracle_f(xn, fh, cfg.M, 2.0, m, window)["f"]) <= TOL[prec]
+    p0.close()
+    p1.close()
+
+
+def test_precompute_psi_unsupported(bn):
+    for d, batch in ((2, 1), (3, 1), (1, 4)):
+        with pytest.raises(bn.BnfftError) as ei:
+            bn.Plan(d, 64, 2.0, 4, "sinh", "c64", batch=batch, precompute_psi=True)
+        assert ei.value.code == bn.BNFFT_E_UNSUPPORTED
