@@ -15,7 +15,8 @@ static bool use_coop3(const bnfft_plan_s* p) {
   return p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
 }
 
-static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false) {
+static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false, bool pre = false) {
+  if (d == 1 && pre && !batched) return c128 ? gather_kernel_1d(m + 300, poly) : gather_kernel_1f(m + 300, poly);
   if (d == 3 && m == 4 && !c128 && !batched) return poly ? gather3c_kernel_p() : gather3c_kernel_e();
   if (d == 1 && batched) return c128 ? gather_kernel_1d(m + 100, poly) : gather_kernel_1f(m + 100, poly);
   if (d == 1) return c128 ? gather_kernel_1d(m, poly) : gather_kernel_1f(m, poly);
@@ -128,7 +129,8 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
 constexpr int kMaxSegPerRound = 32;
 
 cudaError_t gather_prepare(bnfft_plan_s* p) {
-  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1);
+  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1,
+                                 (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0);
   if (!fn) return cudaErrorInvalidValue;
   if (p->opts.d == 1 && p->opts.batch == 1) {
     // two contiguous windows (double buffer) of 12 KB each; persistent grid sized by occupancy
@@ -145,6 +147,10 @@ cudaError_t gather_prepare(bnfft_plan_s* p) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGatherThreads, p->gather_smem);
     if (e != cudaSuccess) return e;
+    if (const char* s = getenv("BNFFT_GATHER1_CTAS_PER_SM")) {   // tuning knob
+      const int v = atoi(s);
+      if (v >= 1 && v < per_sm) per_sm = v;
+    }
     p->gather_grid1 = (int64_t)std::max(1, per_sm) * nsm;
     return cudaSuccess;
   }
@@ -241,7 +247,8 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
 
 cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
   if (p->n == 0) return cudaSuccess;
-  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1);
+  const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1,
+                                 (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0);
   if (!fn) return cudaErrorInvalidValue;
   return p->c128 ? launch_gather_t<double>(p, out, fn) : launch_gather_t<float>(p, out, fn);
 }

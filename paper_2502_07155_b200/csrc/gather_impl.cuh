@@ -523,7 +523,7 @@ struct PreStride {
   static constexpr int v = (T + V - 1) / V * V;
 };
 
-template <int T, typename R, bool POLY>
+template <int T, typename R, bool POLY, bool PRE = false>
 __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_constant__ GatherParams<R> p) {
   using C = typename CT<R>::C;
   constexpr int NPT = NPT1<R>::v;
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_co
       double u;
       if (!node_cell(cur.x[j], p.Lf, p.L, c, u)) continue;
       R w[T];
-      if (p.pre_w) {   // Algorithm 2 step 0(b): weights precomputed by set_nodes
+      if constexpr (PRE) {   // Algorithm 2 step 0(b): weights precomputed by set_nodes
         const int64_t i = k * (int64_t)kGatherThreads * NPT + j * kGatherThreads + threadIdx.x;
         const R* src = p.pre_w + i * PreStride<T, R>::v;
 #pragma unroll
@@ -615,7 +615,8 @@ __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_co
 }
 
 // D == 1: the pipelined window kernel (batch == 1) or, for batched d = 1 plans, the generic
-// segment kernel (returned for m + 100).
+// segment kernel (returned for m + 100); m + 200: the step 0(b) weight kernel, m + 300: the window
+// kernel reading those weights.
 // d = 2, 3 gather: persistent CTAs over the sort keys (user block, bin), TMA tensor staging.
 //
 // Work item = (key u, batch slice s).  The bin's grid neighbourhood (bin + (m-1, m) halo) is one box
@@ -971,6 +972,7 @@ static const void* kernel_for(int m) {
   if constexpr (D == 1) {
     if (m == MM + 100) return (const void*)gather_kernel<1, 2 * MM, R, POLY>;
     if (m == MM + 200) return (const void*)prepsi1_kernel<2 * MM, R, POLY>;
+    if (m == MM + 300) return (const void*)gather1_kernel<2 * MM, R, POLY, true>;
   }
   if constexpr (MM > 1) return kernel_for<D, R, POLY, MM - 1>(m);
   return nullptr;

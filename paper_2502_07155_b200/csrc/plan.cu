@@ -319,12 +319,14 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
       int64_t per = (int64_t)o->batch * (int64_t)p->csize;
       int ub = kSortTileLog2;
       while (ub < 31 && (((int64_t)1 << (ub + 1)) * per) <= ((int64_t)16 << 20)) ++ub;
+      if (const char* s = getenv("BNFFT_UB_LOG2")) ub = atoi(s);
       ub = std::max(ub, kSortTileLog2);   // user blocks are whole sort tiles
-      p->ub_log2 = ub;
+      p->ub_log2 = std::min(ub, 31);
     } else {
       p->ub_log2 = 31;
     }
     p->xs_user = p->ub_log2 < 31;
+    if (getenv("BNFFT_XS_SORTED")) p->xs_user = false;
   }
 
   int rc = BNFFT_OK;
