@@ -19,7 +19,7 @@ constexpr int kSortItems = 8;         // keys per thread per tile
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kSortTileLog2 = 12;
 static_assert(kSortTile == (1 << kSortTileLog2), "sort tile is a power of two");
-constexpr int kMaxDigitBits = 8;
+constexpr int kMaxDigitBits = 9;
 constexpr int kQuadN = 64;            // Gauss-Legendre points for psi^ (reading A4)
 
 // Window parameters in grid units tau = L x (|tau| <= m is the support).
@@ -130,6 +130,7 @@ struct bnfft_plan_s {
   int64_t gather_grid1 = 0;   // persistent grid size (SMs x resident CTAs)
   int gather_nslice = 1, gather_box_elems = 0, gather_bufstride = 0;
   int gather_tbox[3] = {1, 1, 1};
+  bool d1_binned = false;         // d = 1: bins of 2^bin_log2 cells, one radix pass, per-bin gather
   void* d_pre_w = nullptr;        // BNFFT_PRECOMPUTE_PSI: [n][2m] weights of the sorted nodes
   int64_t pre_cap = 0;
   alignas(64) CUtensorMap tmap;   // d >= 2: TMA descriptor of the theta grid (host copy)

@@ -15,8 +15,10 @@ static bool use_coop3(const bnfft_plan_s* p) {
   return p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
 }
 
-static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false, bool pre = false) {
+static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false, bool pre = false,
+                                bool binned = false) {
   if (d == 1 && pre && !batched) return c128 ? gather_kernel_1d(m + 300, poly) : gather_kernel_1f(m + 300, poly);
+  if (d == 1 && binned && !batched) return c128 ? gather_kernel_1d(m + 400, poly) : gather_kernel_1f(m + 400, poly);
   if (d == 3 && m == 4 && !c128 && !batched) return poly ? gather3c_kernel_p() : gather3c_kernel_e();
   if (d == 1 && batched) return c128 ? gather_kernel_1d(m + 100, poly) : gather_kernel_1f(m + 100, poly);
   if (d == 1) return c128 ? gather_kernel_1d(m, poly) : gather_kernel_1f(m, poly);
@@ -130,8 +132,30 @@ constexpr int kMaxSegPerRound = 32;
 
 cudaError_t gather_prepare(bnfft_plan_s* p) {
   const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1,
-                                 (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0);
+                                 (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0, p->d1_binned);
   if (!fn) return cudaErrorInvalidValue;
+  if (p->d1_binned) {
+    // one window per bin (bin + halo, 16-byte aligned), double-buffered; persistent grid by occupancy
+    int cap = (1 << p->bin_log2[0]) + 2 * p->opts.m + 2;
+    cap += cap & 1;
+    p->gather_box_cap = cap;
+    p->gather_smem = 2 * (size_t)cap * p->csize;
+    p->gather_bt = 1;
+    p->gather_smax = 1;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, nsm = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGather1bThreads, p->gather_smem);
+    if (e != cudaSuccess) return e;
+    if (const char* s = getenv("BNFFT_GATHER1_CTAS_PER_SM")) {   // tuning knob
+      const int v = atoi(s);
+      if (v >= 1 && v < per_sm) per_sm = v;
+    }
+    p->gather_grid1 = (int64_t)std::max(1, per_sm) * nsm;
+    return cudaSuccess;
+  }
   if (p->opts.d == 1 && p->opts.batch == 1) {
     // two contiguous windows (double buffer) of 12 KB each; persistent grid sized by occupancy
     // window: chunk cells (~256*NPT at density 1) + one bin + halo, capped at 40 KB per buffer
@@ -233,6 +257,12 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
     return e2;
   }
   unsigned blocks;
+  if (p->d1_binned) {
+    blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p->nkeys, p->gather_grid1));
+    cudaError_t eb = cudaLaunchKernel(fn, dim3(blocks), dim3(kGather1bThreads), args, p->gather_smem, p->stream);
+    p->launches++;
+    return eb;
+  }
   if (p->opts.d == 1 && p->opts.batch == 1) {
     const int64_t ch = (int64_t)kGatherThreads * NPT1<R>::v;
     blocks = (unsigned)std::min<int64_t>((p->n + ch - 1) / ch, p->gather_grid1);
@@ -248,7 +278,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
 cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
   if (p->n == 0) return cudaSuccess;
   const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1,
-                                 (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0);
+                                 (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0, p->d1_binned);
   if (!fn) return cudaErrorInvalidValue;
   return p->c128 ? launch_gather_t<double>(p, out, fn) : launch_gather_t<float>(p, out, fn);
 }

@@ -614,6 +614,123 @@ __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_co
   }
 }
 
+// ---- d = 1, batch 1, large grids (plan.d1_binned): bins of W = 2^bin_log2 cells, so the sort key
+// (user block, bin) is a single radix digit.  Work item = one key: its nodes [key_start[k],
+// key_start[k+1]) and the fixed window [bin*W - m + 1, bin*W + W + m) (16-byte aligned; zero outside
+// I_L, reading A5, or wrapped for Algorithm 1).  Persistent CTAs take keys k = blockIdx.x + j*gridDim;
+// the window of the CTA's next key is in flight (TMA bulk copy, mbarrier) while the current key's
+// nodes are contracted, 256 * NPT at a time with the next batch's node data prefetched into registers.
+template <typename R, int NPT, int NT>
+__device__ __forceinline__ void load_nodes_range(const GatherParams<R>& p, int64_t base, int64_t end,
+                                                 NodeSet1<R, NPT>& ns) {
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const int64_t i = base + j * NT + threadIdx.x;
+    if (i < end) {
+      ns.dst[j] = __ldg(&p.perm[i]);
+      ns.x[j] = __ldg(&p.xs[p.xs_user ? (int64_t)ns.dst[j] : i]);
+    } else {
+      ns.x[j] = 2.0;   // inactive slot
+      ns.dst[j] = 0;
+    }
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ int64_t bin_window_lo(const GatherParams<R>& p, int64_t bin, int m) {
+  constexpr int EPV = 16 / (int)sizeof(typename CT<R>::C);
+  int64_t lo = (bin << p.log2W[0]) - (m - 1);
+  lo -= ((lo % EPV) + EPV) % EPV;
+  return lo;
+}
+
+// thread 0 issues the TMA copies of key k's window into buf (expect_tx on bar); all threads zero-fill
+// the parts outside I_L (non-periodic).  Returns false for an empty key (nothing issued).
+template <typename R, int NT>
+__device__ __forceinline__ bool issue_bin_window(const GatherParams<R>& p, int64_t k, int m,
+                                                 typename CT<R>::C* buf, uint64_t* bar) {
+  using C = typename CT<R>::C;
+  if (__ldg(&p.key_start[k + 1]) == __ldg(&p.key_start[k])) return false;
+  const int64_t bin = k % p.nb[0];
+  const int64_t lo = bin_window_lo(p, bin, m);
+  const int64_t hi = lo + p.boxcap;
+  const int64_t g0 = lo > 0 ? lo : (int64_t)0, g1 = hi < p.L ? hi : p.L;
+  const bool periodic = p.wp.alg1 != 0;
+  if (threadIdx.x == 0) {
+    const int64_t wlo = periodic ? (g0 - lo) : 0, whi = periodic ? (hi - g1) : 0;
+    mbar_expect_tx(bar, (uint32_t)((g1 - g0 + wlo + whi) * (int64_t)sizeof(C)));
+    if (g1 > g0) tma_bulk_g2s(buf + (g0 - lo), (const C*)p.grid + g0, (uint32_t)((g1 - g0) * sizeof(C)), bar);
+    if (wlo) tma_bulk_g2s(buf, (const C*)p.grid + (lo + p.L), (uint32_t)(wlo * sizeof(C)), bar);
+    if (whi) tma_bulk_g2s(buf + (g1 - lo), (const C*)p.grid, (uint32_t)(whi * sizeof(C)), bar);
+  }
+  if (!periodic) {
+    for (int64_t q = threadIdx.x; q < g0 - lo; q += NT) buf[q] = czero<C>();
+    for (int64_t q = (g1 - lo) + threadIdx.x; q < hi - lo; q += NT) buf[q] = czero<C>();
+  }
+  return true;
+}
+
+constexpr int kGather1bThreads = 512;
+
+template <int T, typename R, bool POLY>
+__global__ void __launch_bounds__(kGather1bThreads) gather1b_kernel(const __grid_constant__ GatherParams<R> p) {
+  using C = typename CT<R>::C;
+  constexpr int NPT = NPT1<R>::v;
+  constexpr int m = T / 2;
+  constexpr int NT = kGather1bThreads;
+  constexpr int64_t CHN = (int64_t)NT * NPT;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  C* buf0 = reinterpret_cast<C*>(smem_raw);
+  C* buf1 = buf0 + p.boxcap;
+  __shared__ __align__(8) uint64_t bars[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  C* __restrict__ out = (C*)p.out;
+  const int64_t G = gridDim.x;
+  int64_t k = blockIdx.x;
+  if (k < p.nkeys) issue_bin_window<R, NT>(p, k, m, buf0, &bars[0]);
+  __syncthreads();   // zero-fill of the first window visible
+  uint32_t phases = 0u;
+  for (int it = 0; k < p.nkeys; ++it, k += G) {
+    const int b = it & 1;
+    C* bcur = b ? buf1 : buf0;
+    const int64_t s0 = __ldg(&p.key_start[k]), s1 = __ldg(&p.key_start[k + 1]);
+    NodeSet1<R, NPT> cur, nxt;
+    if (s1 > s0) load_nodes_range<R, NPT, NT>(p, s0, s1, cur);
+    // next key's window into the other buffer (its previous user finished before the barrier that
+    // ended the previous iteration)
+    if (k + G < p.nkeys) issue_bin_window<R, NT>(p, k + G, m, b ? buf0 : buf1, &bars[b ^ 1]);
+    if (s1 > s0) {
+      mbar_wait(&bars[b], (phases >> b) & 1u);
+      phases ^= 1u << b;
+      const int64_t lo = bin_window_lo(p, k % p.nb[0], m);
+      for (int64_t base = s0; base < s1; base += CHN) {
+        if (base + CHN < s1) load_nodes_range<R, NPT, NT>(p, base + CHN, s1, nxt);
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) {
+          int c;
+          double u;
+          if (!node_cell(cur.x[j], p.Lf, p.L, c, u)) continue;
+          const DimState<R> st = dim_state<T, R, POLY>(u, p);
+          R w[T];
+          all_taps<T, POLY>(st, p, w);
+          C acc = czero<C>();
+          const C* row = bcur + (c - (m - 1) - lo);
+#pragma unroll
+          for (int kk = 0; kk < T; ++kk) cmac(acc, w[kk], row[kk]);
+          out[cur.dst[j]] = acc;
+        }
+        cur = nxt;
+      }
+    }
+    __syncthreads();   // every thread done with buffer b (and the next window's zero-fill visible)
+  }
+}
+
 // D == 1: the pipelined window kernel (batch == 1) or, for batched d = 1 plans, the generic
 // segment kernel (returned for m + 100); m + 200: the step 0(b) weight kernel, m + 300: the window
 // kernel reading those weights.
@@ -973,6 +1090,7 @@ static const void* kernel_for(int m) {
     if (m == MM + 100) return (const void*)gather_kernel<1, 2 * MM, R, POLY>;
     if (m == MM + 200) return (const void*)prepsi1_kernel<2 * MM, R, POLY>;
     if (m == MM + 300) return (const void*)gather1_kernel<2 * MM, R, POLY, true>;
+    if (m == MM + 400) return (const void*)gather1b_kernel<2 * MM, R, POLY>;
   }
   if constexpr (MM > 1) return kernel_for<D, R, POLY, MM - 1>(m);
   return nullptr;

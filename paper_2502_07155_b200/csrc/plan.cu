@@ -296,6 +296,19 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   if (o->d == 3) lg = o->batch > 1 ? 2 : 3;
   int lgL = 0;
   while (((int64_t)1 << (lgL + 1)) <= L) ++lgL;
+  // d = 1, batch 1, large grids: bins wide enough that the key (bin index) fits one radix digit, when
+  // a bin's window (bin + halo) fits the per-CTA double buffer; the gather then walks whole bins
+  // (gather1b).  Otherwise 128-cell bins and the chunked window kernel.
+  p->d1_binned = false;
+  if (o->d == 1 && o->batch == 1 && !(o->flags & BNFFT_PRECOMPUTE_PSI) && lgL - lg > kMaxDigitBits &&
+      !getenv("BNFFT_D1_CHUNKED")) {
+    const int lgb = lgL - kMaxDigitBits;
+    const size_t win = (((size_t)1 << lgb) + 2 * (size_t)o->m + 2) * (size_t)p->csize;
+    if (win <= ((size_t)40 << 10)) {
+      lg = lgb;
+      p->d1_binned = true;
+    }
+  }
   lg = std::min(lg, lgL);
   int64_t nbins = 1;
   // d = 3, m = 4, complex64, batch 1 (warp-cooperative gather): bins of 8 x 8 x 16 cells, so the
@@ -496,7 +509,7 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
     timer_end(p, ST_BUILD, ev);
   }
   p->offsets_valid = false;
-  if (p->opts.d >= 2) {   // key offsets for the binned gather (d = 1 builds them on demand)
+  if (p->opts.d >= 2 || p->d1_binned) {   // key offsets for the binned gathers (else built on demand)
     timer_begin(p, ST_BUILD, &ev);
     if ((e = launch_build(p, x, n)) != cudaSuccess) return cuda_fail(e, "build kernel");
     timer_end(p, ST_BUILD, ev);

@@ -417,7 +417,8 @@ static ScatterFn scatter_for(int bits) {
     case 5: return radix_scatter_kernel<5>;
     case 6: return radix_scatter_kernel<6>;
     case 7: return radix_scatter_kernel<7>;
-    default: return radix_scatter_kernel<8>;
+    case 8: return radix_scatter_kernel<8>;
+    default: return radix_scatter_kernel<9>;
   }
 }
 
@@ -468,7 +469,34 @@ cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n) {
   return cudaGetLastError();
 }
 
+// Key offsets of a one-pass sort straight from the scanned digit histogram: with the whole key as
+// the digit, the first sorted position of key (block, bin) is the scanned count of the block's first
+// tile for digit `bin` (digit-major layout inside a block, hist_index).
+__global__ void offsets_from_hist_kernel(const uint32_t* __restrict__ hist_scan, SegLayout sl, int ndig,
+                                         int64_t nbins, int64_t nkeys, int64_t n,
+                                         uint32_t* __restrict__ key_start) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= nkeys;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (k == nkeys) {
+      key_start[k] = (uint32_t)n;
+    } else {
+      const int64_t blk = k / nbins;
+      const int dg = (int)(k - blk * nbins);
+      key_start[k] = hist_scan[hist_index(sl, blk * sl.tpb, dg, ndig)];
+    }
+  }
+}
+
 cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n) {
+  if (p->sort_passes == 1 && n > 0) {
+    SegLayout sl;
+    sl.ntiles = (n + kSortTile - 1) / kSortTile;
+    sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - kSortTileLog2));
+    offsets_from_hist_kernel<<<grid_for(p->nkeys + 1, 256), 256, 0, p->stream>>>(
+        p->d_hist, sl, 1 << p->digit_bits, p->nbins, p->nkeys, n, p->d_bin_start);
+    p->launches++;
+    return cudaGetLastError();
+  }
   build_kernel<<<grid_for(n + 1, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys,
                                                             nullptr,   // xs comes from the sort
                                                             p->d_bin_start, n, p->opts.d,
