@@ -331,7 +331,8 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     if (o->d <= 2 && gbytes_one <= ((int64_t)48 << 20)) {
       int64_t per = (int64_t)o->batch * (int64_t)p->csize;
       int ub = kSortTileLog2;
-      while (ub < 31 && (((int64_t)1 << (ub + 1)) * per) <= ((int64_t)16 << 20)) ++ub;
+      const int64_t target = p->d1_binned ? ((int64_t)8 << 20) : ((int64_t)16 << 20);   // measured (cfg2)
+      while (ub < 31 && (((int64_t)1 << (ub + 1)) * per) <= target) ++ub;
       if (const char* s = getenv("BNFFT_UB_LOG2")) ub = atoi(s);
       ub = std::max(ub, kSortTileLog2);   // user blocks are whole sort tiles
       p->ub_log2 = std::min(ub, 31);
@@ -448,7 +449,7 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
   if (n > p->cap) {
     free_nodes(p);
     int64_t cap = std::max<int64_t>(n, 1);
-    size_t b4 = cap * sizeof(uint32_t);
+    size_t b4 = (cap + 4) * sizeof(uint32_t);   // +4: 16-byte bulk copies of permutation ranges
     if ((e = dmalloc(p, &p->d_xs, cap * p->opts.d * sizeof(double))) != cudaSuccess ||
         (e = dmalloc(p, &p->d_k0, b4)) != cudaSuccess || (e = dmalloc(p, &p->d_k1, b4)) != cudaSuccess ||
         (e = dmalloc(p, &p->d_v0, b4)) != cudaSuccess || (e = dmalloc(p, &p->d_v1, b4)) != cudaSuccess)

@@ -24,6 +24,17 @@ struct KeyParams {
 
 enum { BAD_NOT_FINITE = 1, BAD_RANGE = 2, BAD_BOX = 3 };
 
+struct SegLayout {
+  int64_t tpb;      // tiles per user block
+  int64_t ntiles;
+};
+__device__ __forceinline__ int64_t hist_index(const SegLayout& sl, int64_t tile, int dg, int ndig) {
+  const int64_t blk = tile / sl.tpb;
+  const int64_t tib = tile - blk * sl.tpb;
+  const int64_t tin = min(sl.tpb, sl.ntiles - blk * sl.tpb);
+  return blk * sl.tpb * ndig + (int64_t)dg * tin + tib;
+}
+
 // K1: validate + key.  bad = min over nodes of (index << 4 | code).  Each thread handles a pair of
 // consecutive nodes with 16-byte loads/stores (2*D doubles, 2 keys).
 template <int D>
@@ -96,21 +107,82 @@ __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams k
   }
 }
 
+// K1 + K2a of the first radix pass: one CTA per sort tile (kSortTile nodes, kSortItems/2 node pairs
+// per thread) validates, keys and copies its nodes as keys_kernel does and also counts the tile's
+// first-pass digits (shared-memory integer counts: order-free) into the block-major histogram.
+template <int D>
+__global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(
+    const double* __restrict__ x, int64_t n, KeyParams kp, uint32_t* __restrict__ keys,
+    unsigned long long* __restrict__ bad, double* __restrict__ xcopy, int aligned16, int bits,
+    uint32_t* __restrict__ hist, SegLayout sl) {
+  __shared__ uint32_t cnt[1 << kMaxDigitBits];
+  const int ndig = 1 << bits;
+  const uint32_t mask = ndig - 1;
+  for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x) cnt[dgt] = 0;
+  __syncthreads();
+  const int64_t q0 = (int64_t)blockIdx.x * (kSortTile / 2);
+  constexpr int NP = kSortItems / 2;
+  double xv[NP][2 * D];
+  // all loads first (independent, in flight together)
+#pragma unroll
+  for (int jj = 0; jj < NP; ++jj) {
+    const int64_t i = 2 * (q0 + jj * kSortThreads + threadIdx.x);
+    const bool full = i + 1 < n;
+    if (full && aligned16) {
+      const double2* src = reinterpret_cast<const double2*>(x + i * D);
+#pragma unroll
+      for (int h = 0; h < D; ++h) {
+        const double2 v = __ldg(&src[h]);
+        xv[jj][2 * h] = v.x;
+        xv[jj][2 * h + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 2 * D; ++t) {
+        const bool in = i < n && (t < D || full);
+        xv[jj][t] = in ? __ldg(&x[i * D + t]) : 0.0;
+      }
+    }
+  }
+#pragma unroll
+  for (int jj = 0; jj < NP; ++jj) {
+    const int64_t q = q0 + jj * kSortThreads + threadIdx.x;
+    const int64_t i = 2 * q;
+    if (i >= n) continue;
+    const bool full = i + 1 < n;
+    if (xcopy) {
+      if (full && aligned16) {
+        double2* dstc = reinterpret_cast<double2*>(xcopy + i * D);
+#pragma unroll
+        for (int h = 0; h < D; ++h) dstc[h] = make_double2(xv[jj][2 * h], xv[jj][2 * h + 1]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 2 * D; ++t)
+          if (t < D || full) xcopy[i * D + t] = xv[jj][t];
+      }
+    }
+    int c0 = 0, c1 = 0;
+    const uint32_t k0 = node_key<D>(xv[jj], kp, c0);
+    const uint32_t k1 = full ? node_key<D>(xv[jj] + D, kp, c1) : 0u;
+    if (c0) atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)c0);
+    if (c1) atomicMin(bad, ((unsigned long long)(i + 1) << 4) | (unsigned long long)c1);
+    atomicAdd(&cnt[k0 & mask], 1u);
+    if (full) {
+      atomicAdd(&cnt[k1 & mask], 1u);
+      reinterpret_cast<uint2*>(keys)[q] = make_uint2(k0, k1);
+    } else {
+      keys[i] = k0;
+    }
+  }
+  __syncthreads();
+  for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x)
+    hist[hist_index(sl, blockIdx.x, dgt, ndig)] = cnt[dgt];
+}
+
 // Sort key = (user block, bin): the input is in user order, so the user-block part of the key is
 // already sorted; the radix passes run over the bin digits only, with the per-tile histograms laid
 // out block-major so that the scan never moves an element across a user block:
 //   hist[blk*tpb*ndig + dg*tiles_in(blk) + tile_in_blk]      (scan order = (blk, digit, tile)).
-struct SegLayout {
-  int64_t tpb;      // tiles per user block
-  int64_t ntiles;
-};
-__device__ __forceinline__ int64_t hist_index(const SegLayout& sl, int64_t tile, int dg, int ndig) {
-  const int64_t blk = tile / sl.tpb;
-  const int64_t tib = tile - blk * sl.tpb;
-  const int64_t tin = min(sl.tpb, sl.ntiles - blk * sl.tpb);
-  return blk * sl.tpb * ndig + (int64_t)dg * tin + tib;
-}
-
 // K2a: per-tile digit histogram.
 __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(
     const uint32_t* __restrict__ keys, int64_t n, int shift, int bits,
@@ -166,13 +238,33 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total)
   return before;
 }
 
+// kScanItems consecutive entries from base (a multiple of kScanItems): 16-byte loads when complete
+__device__ __forceinline__ void load_items(const uint32_t* __restrict__ in, int64_t base, int64_t n,
+                                           uint32_t (&v)[kScanItems]) {
+  if (base + kScanItems <= n) {
+    const uint4* src = reinterpret_cast<const uint4*>(in + base);
+#pragma unroll
+    for (int j = 0; j < kScanItems / 4; ++j) {
+      const uint4 q = src[j];
+      v[4 * j] = q.x;
+      v[4 * j + 1] = q.y;
+      v[4 * j + 2] = q.z;
+      v[4 * j + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) v[j] = (base + j < n) ? in[base + j] : 0u;
+  }
+}
+
 __global__ void __launch_bounds__(256) scan_reduce_kernel(const uint32_t* __restrict__ in,
                                                           int64_t n, uint32_t* __restrict__ part) {
   const int64_t base = (int64_t)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  load_items(in, base, n, v);
   uint32_t s = 0;
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j)
-    if (base + j < n) s += in[base + j];
+  for (int j = 0; j < kScanItems; ++j) s += v[j];
   uint32_t tot;
   block_excl_scan(s, &tot);
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
@@ -206,18 +298,26 @@ __global__ void __launch_bounds__(256) scan_down_kernel(const uint32_t* __restri
                                                         uint32_t* __restrict__ out) {
   const int64_t base = (int64_t)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
+  load_items(in, base, n, v);
   uint32_t s = 0;
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    v[j] = (base + j < n) ? in[base + j] : 0;
-    s += v[j];
-  }
+  for (int j = 0; j < kScanItems; ++j) s += v[j];
   uint32_t tot;
   uint32_t run = part[blockIdx.x] + block_excl_scan(s, &tot);
+  uint32_t o[kScanItems];
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    if (base + j < n) out[base + j] = run;
+    o[j] = run;
     run += v[j];
+  }
+  if (base + kScanItems <= n) {   // 16-byte stores (base is a multiple of 16 elements)
+    uint4* dst = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+    for (int j = 0; j < kScanItems / 4; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j)
+      if (base + j < n) out[base + j] = o[j];
   }
 }
 
@@ -340,7 +440,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     uint32_t kk = skey[li];
     uint32_t dg = (kk >> shift) & mask;
     uint32_t pos = gbase[dg] + (uint32_t)li - tstart[dg];
-    kout[pos] = kk;
+    if (kout) kout[pos] = kk;   // null: sorted keys not needed (one-pass sort, offsets from the histogram)
     const uint32_t vv = sval[li];
     vout[pos] = vv;
     if (xsout)
@@ -386,7 +486,17 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
   kp.box_hi = 0.5 - (double)p->opts.m / (double)p->L;
   cudaError_t e = cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), p->stream);
   if (e != cudaSuccess) return e;
-  if (n > 0) {
+  if (n > 0 && p->sort_passes > 0 && p->opts.d <= 2) {   // first-pass histogram fused (d <= 2)
+    SegLayout sl;
+    sl.ntiles = (n + kSortTile - 1) / kSortTile;
+    sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - kSortTileLog2));
+    const int b0 = std::min(p->digit_bits, p->key_bits);
+    auto kfn = p->opts.d == 1 ? keys_hist_kernel<1> : keys_hist_kernel<2>;
+    kfn<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(x, n, kp, p->d_k0, p->d_bad,
+                                                              p->xs_user ? p->d_xs : nullptr,
+                                                              ((uintptr_t)x & 15) == 0 ? 1 : 0, b0, p->d_hist, sl);
+    p->launches++;
+  } else if (n > 0) {
     auto kfn = p->opts.d == 1 ? keys_kernel<1> : p->opts.d == 2 ? keys_kernel<2> : keys_kernel<3>;
     kfn<<<grid_for((n + 1) / 2, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0,
                                                            p->sort_passes ? nullptr : p->d_v0, p->d_bad,
@@ -442,14 +552,17 @@ cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n) {
       int shift = pass * bits;
       int b = std::min(bits, p->key_bits - shift);
       int64_t nh = ((int64_t)1 << b) * sl.ntiles;
-      radix_hist_kernel<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(kin, n, shift, b,
-                                                                             p->d_hist, sl);
-      p->launches++;
+      if (pass > 0 || p->opts.d > 2) {   // d <= 2, pass 0: counted by keys_hist_kernel
+        radix_hist_kernel<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(kin, n, shift, b,
+                                                                               p->d_hist, sl);
+        p->launches++;
+      }
       cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
       if (e != cudaSuccess) return e;
       const bool last = pass == p->sort_passes - 1;
       scatter_for(b)<<<(unsigned)sl.ntiles, kSortThreads, 2 * kSortTile * sizeof(uint32_t), p->stream>>>(
-          kin, vin, kout, vout, n, shift, p->d_hist, sl, x, (last && !p->xs_user) ? p->d_xs : nullptr,
+          kin, vin, (last && p->sort_passes == 1) ? nullptr : kout, vout, n, shift, p->d_hist, sl, x,
+          (last && !p->xs_user) ? p->d_xs : nullptr,
           p->opts.d);
       p->launches++;
       std::swap(kin, kout);
