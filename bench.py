@@ -36,13 +36,9 @@ import synth  # noqa: E402
 
 
 
-def gather_kernel_name(cfg, prec):
-    """The gather kernel the library dispatches for this workload (gather.cu select_kernel)."""
-    if cfg.d == 1:
-        return "bnfft::gather1_kernel" if cfg.batch == 1 else "bnfft::gather_kernel"
-    if cfg.d == 3 and cfg.m == 4 and prec == "c64" and cfg.batch == 1:
-        return "bnfft::gather3c_kernel"
-    return "bnfft::gatherN_kernel"
+def gather_kernel_name(bn, info):
+    """The gather kernel the library dispatches for this plan (bnfft_info.gather_kernel)."""
+    return bn.GATHER_KERNELS.get(int(info.gather_kernel), "unknown")
 
 
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
@@ -282,10 +278,14 @@ def run_gpu(args):
         g_ms = stages["gather"]
         achieved = bpn * cfg.N / (g_ms * 1e-3) / 1e9
         traffic = None
+        kname = gather_kernel_name(bn, info)
         tpath = os.path.join(ROOT, "profiles", f"ncu_gather_cfg{cfg.cfg_id}_{window}_{prec}.json")
         if os.path.exists(tpath):
             try:
-                traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+                tj = json.load(open(tpath))
+                # only a capture of the kernel this build dispatches counts
+                if kname.split("::")[-1] in tj.get("kernel", ""):
+                    traffic = tj.get("dram_bytes_per_launch")
             except Exception:
                 traffic = None
         line = {
@@ -295,7 +295,7 @@ def run_gpu(args):
             "vs_baseline": None, "dtype": "f64" if prec == "c128" else "f32",
             "data": "synthetic (seeded, synth/; BASELINE configs recipe)",
             "config": dict(describe(cfg, prec, window), parallelism=f"replicas{world}"),
-            "roofline": {"bound": "hbm", "kernel": gather_kernel_name(cfg, prec),
+            "roofline": {"bound": "hbm", "kernel": kname,
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "bytes_per_node": bpn, "peak_source": hbm_src,

@@ -131,7 +131,18 @@ typedef struct {
   int64_t n_nodes;          /* nodes of the last successful set_nodes (0 if none)          */
   int64_t grid_bytes;       /* bytes of one theta grid (batch x L^d complex)               */
   int64_t device_bytes;     /* device memory currently owned by the plan                   */
+  int32_t gather_kernel;    /* step-3 kernel execute launches: BNFFT_GK_*                  */
 } bnfft_info;
+
+/* bnfft_info.gather_kernel */
+enum {
+  BNFFT_GK_WINDOW1 = 0,   /* d = 1: chunked window kernel (gather1_kernel)                 */
+  BNFFT_GK_BIN1 = 1,      /* d = 1, large grids: per-bin kernel (gather1b_kernel)           */
+  BNFFT_GK_SEGMENT = 2,   /* d = 1 batched: generic segment kernel (gather_kernel)          */
+  BNFFT_GK_BOX = 3,       /* d = 2, 3: binned TMA-box kernel (gatherN_kernel)               */
+  BNFFT_GK_COOP3 = 4,     /* d = 3, m = 4, complex64: warp-cooperative kernel (gather3c)    */
+  BNFFT_GK_PRE1 = 5       /* d = 1 with BNFFT_PRECOMPUTE_PSI (gather1_kernel, stored taps)  */
+};
 
 /* Per-stage device times (ms) accumulated since the last reset, and call counts.  Only
  * recorded with BNFFT_TIMING.  Events are recorded on the plan's stream around each stage's

@@ -54,7 +54,12 @@ class bnfft_info(ctypes.Structure):
                 ("bin_log2", c_int32 * 3), ("bins_per_dim", c_int64 * 3), ("nbins", c_int64),
                 ("user_block_log2", c_int32), ("nkeys", c_int64), ("tap_poly", c_int32),
                 ("tap_fit_err", c_double), ("key_bits", c_int32), ("sort_passes", c_int32), ("flatness", c_double),
-                ("n_nodes", c_int64), ("grid_bytes", c_int64), ("device_bytes", c_int64)]
+                ("n_nodes", c_int64), ("grid_bytes", c_int64), ("device_bytes", c_int64),
+                ("gather_kernel", c_int32)]
+
+
+GATHER_KERNELS = {0: "bnfft::gather1_kernel", 1: "bnfft::gather1b_kernel", 2: "bnfft::gather_kernel",
+                  3: "bnfft::gatherN_kernel", 4: "bnfft::gather3c_kernel", 5: "bnfft::gather1_kernel"}
 
 
 class bnfft_timing(ctypes.Structure):

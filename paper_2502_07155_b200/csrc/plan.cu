@@ -656,6 +656,14 @@ int bnfft_get_info(const bnfft_plan_s* p, bnfft_info* o) {
   o->n_nodes = p->nodes_set ? p->n : 0;
   o->grid_bytes = p->Ld * p->opts.batch * (int64_t)p->csize;
   o->device_bytes = p->device_bytes;
+  if (p->opts.d == 1) {
+    o->gather_kernel = p->opts.batch > 1 ? BNFFT_GK_SEGMENT
+                       : (p->opts.flags & BNFFT_PRECOMPUTE_PSI) ? BNFFT_GK_PRE1
+                       : p->d1_binned ? BNFFT_GK_BIN1 : BNFFT_GK_WINDOW1;
+  } else {
+    o->gather_kernel = (p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1) ? BNFFT_GK_COOP3
+                                                                                            : BNFFT_GK_BOX;
+  }
   return BNFFT_OK;
 }
 

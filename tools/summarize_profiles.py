@@ -21,7 +21,7 @@ def last_json_line(path):
     return None
 
 
-for name in ["bench"] + [f"bench_cfg{c}" for c in (3, 4, 5)]:
+for name in ["bench", "bench_reference"] + [f"bench_cfg{c}" for c in (3, 4, 5)]:
     p = os.path.join(src, f"{tag}_{name}.json")
     if os.path.exists(p):
         d = last_json_line(p)
