@@ -356,26 +356,30 @@ def run_gpu(args):
         line["variants"] = var
         # fixed nodes, repeated transforms (paper step 0(b), BNFFT_PRECOMPUTE_PSI): execute-only rates
         rep = {}
-        for name, kw in (("default", {}), ("precompute_psi", {"precompute_psi": True})):
-            p3 = bn.Plan(cfg.d, cfg.M, cfg.sigma, cfg.m, window, prec, batch=cfg.batch, timing=True,
-                         device=local, stream=stream.cuda_stream, **kw)
-            p3.set_nodes(x_dev)
-            for _ in range(3):
-                p3.execute(fh_dev, out)
-            torch.cuda.synchronize()
-            t_set = p3.timing()
-            p3.reset_timing()
-            a3, b3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a3.record(stream)
-            for _ in range(20):
-                p3.execute(fh_dev, out)
-            b3.record(stream)
-            torch.cuda.synchronize()
-            t3 = p3.timing()
-            rep[name] = {"execute_nodes_per_s": cfg.N / (a3.elapsed_time(b3) / 20 * 1e-3),
-                         "gather_ms": t3.ms_gather / 20,
-                         "set_nodes_ms": t_set.ms_keys + t_set.ms_sort + t_set.ms_build}
-            p3.close()
+        for rp in ("c64", "c128"):
+            fh_r = torch.from_numpy(synth.make_spectrum(cfg, prec=rp)).to(dev)
+            for name, kw in (("default", {}), ("precompute_psi", {"precompute_psi": True})):
+                p3 = bn.Plan(cfg.d, cfg.M, cfg.sigma, cfg.m, window, rp, batch=cfg.batch, timing=True,
+                             device=local, stream=stream.cuda_stream, **kw)
+                out3 = torch.empty((cfg.batch, cfg.N), dtype=p3.cdtype, device=dev)
+                p3.set_nodes(x_dev)
+                for _ in range(3):
+                    p3.execute(fh_r, out3)
+                torch.cuda.synchronize()
+                t_set = p3.timing()
+                p3.reset_timing()
+                a3, b3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a3.record(stream)
+                for _ in range(20):
+                    p3.execute(fh_r, out3)
+                b3.record(stream)
+                torch.cuda.synchronize()
+                t3 = p3.timing()
+                rep[f"{name}-{rp}"] = {"execute_nodes_per_s": cfg.N / (a3.elapsed_time(b3) / 20 * 1e-3),
+                                       "gather_ms": t3.ms_gather / 20,
+                                       "set_nodes_ms": t_set.ms_keys + t_set.ms_sort + t_set.ms_build}
+                p3.close()
+                del out3
         line["repeated_execute"] = rep
 
     # ---- CPU oracle on this box's host cores (rank 0, N=1 only)

@@ -339,7 +339,8 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     } else {
       p->ub_log2 = 31;
     }
-    p->xs_user = p->ub_log2 < 31;
+    // d = 1 one-pass plans: the single radix pass also writes the sorted node copy (radix1x)
+    p->xs_user = p->ub_log2 < 31 && !p->d1_binned;
     if (getenv("BNFFT_XS_SORTED")) p->xs_user = false;
   }
 

@@ -167,11 +167,10 @@ __global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(
     if (c0) atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)c0);
     if (c1) atomicMin(bad, ((unsigned long long)(i + 1) << 4) | (unsigned long long)c1);
     atomicAdd(&cnt[k0 & mask], 1u);
-    if (full) {
-      atomicAdd(&cnt[k1 & mask], 1u);
-      reinterpret_cast<uint2*>(keys)[q] = make_uint2(k0, k1);
-    } else {
-      keys[i] = k0;
+    if (full) atomicAdd(&cnt[k1 & mask], 1u);
+    if (keys) {   // null: the one-pass d = 1 scatter recomputes the keys from x
+      if (full) reinterpret_cast<uint2*>(keys)[q] = make_uint2(k0, k1);
+      else keys[i] = k0;
     }
   }
   __syncthreads();
@@ -472,7 +471,113 @@ static int grid_for(int64_t n, int threads) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148LL * 32));
 }
 
-cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
+// K2b for d = 1 one-pass plans (d1_binned): the keys are recomputed from x (exactly as K1 computed
+// the histogram's), ranked stably per tile like radix_scatter_kernel, and the tile is reordered in
+// shared memory together with its node coordinates, so one pass writes both the permutation and the
+// sorted node copy in digit runs (the gather then streams x instead of gathering it).
+template <int BITS>
+__global__ void __launch_bounds__(kSortThreads) radix1x_scatter_kernel(
+    const double* __restrict__ x, int64_t n, KeyParams kp, const uint32_t* __restrict__ hist_scan,
+    SegLayout sl, uint32_t* __restrict__ perm_out, double* __restrict__ xs_out) {
+  constexpr int kWarps = kSortThreads / 32;
+  constexpr int kPerWarp = kSortTile / kWarps;
+  constexpr int ndig = 1 << BITS;
+  constexpr uint32_t mask = ndig - 1;
+  __shared__ uint32_t wcnt[kWarps][ndig];
+  __shared__ uint32_t gbase[ndig];
+  __shared__ uint32_t tstart[ndig];
+  __shared__ uint32_t wsum[kWarps];
+  extern __shared__ __align__(16) unsigned char dyn1x[];
+  double* sx = reinterpret_cast<double*>(dyn1x);                     // [kSortTile], tile order
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(sx + kSortTile);      // [kSortTile], sorted slot -> tile index
+  uint16_t* sdig = sidx + kSortTile;                                 // [kSortTile], sorted slot -> digit
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kWarps * ndig; i += kSortThreads) wcnt[i / ndig][i % ndig] = 0;
+  {
+    const int64_t h0 = hist_index(sl, blockIdx.x, 0, ndig);
+    const int64_t hs = hist_index(sl, blockIdx.x, 1, ndig) - h0;
+    for (int dgt = threadIdx.x; dgt < ndig; dgt += blockDim.x) gbase[dgt] = hist_scan[h0 + dgt * hs];
+  }
+  const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
+  const int tile_n = (int)min((int64_t)kSortTile, n - tbase);
+  const int wbase = w * kPerWarp;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t k[kSortItems], r[kSortItems];
+  double xv[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {   // all loads first (in flight together)
+    const int li = wbase + j * 32 + lane;
+    xv[j] = li < tile_n ? __ldg(&x[tbase + li]) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int li = wbase + j * 32 + lane;
+    if (li < tile_n) {
+      sx[li] = xv[j];
+      int code;
+      k[j] = node_key<1>(&xv[j], kp, code) & mask;
+    } else {
+      k[j] = 0u;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const bool valid = wbase + j * 32 + lane < tile_n;
+    const uint32_t dg = valid ? k[j] : 0xffffffffu;
+    const uint32_t peers = peers_by_ballot<BITS>(dg, valid);
+    const uint32_t cnt = valid ? wcnt[w][dg] : 0u;
+    r[j] = cnt + __popc(peers & lt_mask);
+    __syncwarp();
+    if (valid) wcnt[w][dg] = cnt + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  uint32_t tcount = 0;
+  const int dg0 = threadIdx.x;
+  if (dg0 < ndig) {
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) {
+      uint32_t t = wcnt[ww][dg0];
+      wcnt[ww][dg0] = tcount;
+      tcount += t;
+    }
+  }
+  uint32_t xs = tcount;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, xs, o);
+    if (lane >= o) xs += y;
+  }
+  if (lane == 31) wsum[w] = xs;
+  __syncthreads();
+  if (dg0 < ndig) {
+    uint32_t before = 0;
+    for (int ww = 0; ww < w; ++ww) before += wsum[ww];
+    tstart[dg0] = before + xs - tcount;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int li = wbase + j * 32 + lane;
+    if (li < tile_n) {
+      const uint32_t dg = k[j];
+      const uint32_t lpos = tstart[dg] + wcnt[w][dg] + r[j];
+      sidx[lpos] = (uint16_t)li;
+      sdig[lpos] = (uint16_t)dg;
+    }
+  }
+  __syncthreads();
+  for (int li = threadIdx.x; li < tile_n; li += kSortThreads) {
+    const uint32_t dg = sdig[li];
+    const uint32_t pos = gbase[dg] + (uint32_t)li - tstart[dg];
+    const uint32_t src = sidx[li];
+    perm_out[pos] = (uint32_t)(tbase + src);
+    xs_out[pos] = sx[src];
+  }
+}
+
+static KeyParams key_params(const bnfft_plan_s* p) {
   KeyParams kp;
   kp.d = p->opts.d;
   kp.L = p->L;
@@ -484,6 +589,13 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
   kp.strict = (p->opts.flags & BNFFT_STRICT_DOMAIN) ? 1 : 0;
   kp.box_lo = -0.5 + (double)p->opts.m / (double)p->L;
   kp.box_hi = 0.5 - (double)p->opts.m / (double)p->L;
+  return kp;
+}
+
+constexpr int kRadix1xSmem = kSortTile * (int)(sizeof(double) + 2 * sizeof(uint16_t));
+
+cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
+  const KeyParams kp = key_params(p);
   cudaError_t e = cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), p->stream);
   if (e != cudaSuccess) return e;
   if (n > 0 && p->sort_passes > 0 && p->opts.d <= 2) {   // first-pass histogram fused (d <= 2)
@@ -492,7 +604,7 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
     sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - kSortTileLog2));
     const int b0 = std::min(p->digit_bits, p->key_bits);
     auto kfn = p->opts.d == 1 ? keys_hist_kernel<1> : keys_hist_kernel<2>;
-    kfn<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(x, n, kp, p->d_k0, p->d_bad,
+    kfn<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(x, n, kp, p->d1_binned ? nullptr : p->d_k0, p->d_bad,
                                                               p->xs_user ? p->d_xs : nullptr,
                                                               ((uintptr_t)x & 15) == 0 ? 1 : 0, b0, p->d_hist, sl);
     p->launches++;
@@ -538,10 +650,30 @@ cudaError_t sort_prepare() {
                                          2 * kSortTile * (int)sizeof(uint32_t));
     if (e != cudaSuccess) return e;
   }
+  for (auto fn : {radix1x_scatter_kernel<7>, radix1x_scatter_kernel<8>, radix1x_scatter_kernel<9>}) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRadix1xSmem);
+    if (e != cudaSuccess) return e;
+  }
   return cudaSuccess;
 }
 
 cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n) {
+  if (p->d1_binned && p->sort_passes == 1 && n > 0) {   // histogram from keys_hist_kernel
+    SegLayout sl;
+    sl.ntiles = (n + kSortTile - 1) / kSortTile;
+    sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - kSortTileLog2));
+    const int64_t nh = ((int64_t)1 << p->key_bits) * sl.ntiles;
+    cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
+    if (e != cudaSuccess) return e;
+    KeyParams kp = key_params(p);
+    auto fn = p->key_bits >= 9 ? radix1x_scatter_kernel<9> : p->key_bits == 8 ? radix1x_scatter_kernel<8>
+                                                                                : radix1x_scatter_kernel<7>;
+    fn<<<(unsigned)sl.ntiles, kSortThreads, kRadix1xSmem, p->stream>>>(x, n, kp, p->d_hist, sl, p->d_v1, p->d_xs);
+    p->launches++;
+    p->d_skeys = nullptr;
+    p->d_perm = p->d_v1;
+    return cudaGetLastError();
+  }
   uint32_t *kin = p->d_k0, *vin = nullptr, *kout = p->d_k1, *vout = p->d_v1;
   if (n > 0 && p->sort_passes > 0) {
     SegLayout sl;
