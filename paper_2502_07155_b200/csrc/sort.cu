@@ -476,14 +476,14 @@ static int grid_for(int64_t n, int threads) {
 // shared memory together with its node coordinates, so one pass writes both the permutation and the
 // sorted node copy in digit runs (the gather then streams x instead of gathering it).
 template <int BITS>
-__global__ void __launch_bounds__(kSortThreads) radix1x_scatter_kernel(
+__global__ void __launch_bounds__(kSortThreads, 3) radix1x_scatter_kernel(
     const double* __restrict__ x, int64_t n, KeyParams kp, const uint32_t* __restrict__ hist_scan,
     SegLayout sl, uint32_t* __restrict__ perm_out, double* __restrict__ xs_out) {
   constexpr int kWarps = kSortThreads / 32;
   constexpr int kPerWarp = kSortTile / kWarps;
   constexpr int ndig = 1 << BITS;
   constexpr uint32_t mask = ndig - 1;
-  __shared__ uint32_t wcnt[kWarps][ndig];
+  __shared__ uint16_t wcnt[kWarps][ndig];   // counts <= kSortTile fit 16 bits (keeps 3 CTAs/SM)
   __shared__ uint32_t gbase[ndig];
   __shared__ uint32_t tstart[ndig];
   __shared__ uint32_t wsum[kWarps];
