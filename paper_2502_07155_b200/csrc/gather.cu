@@ -139,7 +139,7 @@ cudaError_t gather_prepare(bnfft_plan_s* p) {
     int cap = (1 << p->bin_log2[0]) + 2 * p->opts.m + 2;
     cap += cap & 1;
     p->gather_box_cap = cap;
-    p->gather_smem = 2 * (size_t)cap * p->csize;
+    p->gather_smem = (size_t)kGather1bBufs * cap * p->csize;
     p->gather_bt = 1;
     p->gather_smax = 1;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);

@@ -404,6 +404,9 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -623,15 +626,19 @@ __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_co
 template <typename R, int NPT, int NT>
 __device__ __forceinline__ void load_nodes_range(const GatherParams<R>& p, int64_t base, int64_t end,
                                                  NodeSet1<R, NPT>& ns) {
+  if (p.xs_user) {   // user-order node copy: x[perm[i]] (dependent loads)
 #pragma unroll
-  for (int j = 0; j < NPT; ++j) {
-    const int64_t i = base + j * NT + threadIdx.x;
-    if (i < end) {
-      ns.dst[j] = __ldg(&p.perm[i]);
-      ns.x[j] = __ldg(&p.xs[p.xs_user ? (int64_t)ns.dst[j] : i]);
-    } else {
-      ns.x[j] = 2.0;   // inactive slot
-      ns.dst[j] = 0;
+    for (int j = 0; j < NPT; ++j) {
+      const int64_t i = base + j * NT + threadIdx.x;
+      ns.dst[j] = i < end ? __ldg(&p.perm[i]) : 0u;
+      ns.x[j] = i < end ? __ldg(&p.xs[ns.dst[j]]) : 2.0;   // 2.0: inactive slot
+    }
+  } else {            // sorted node copy: independent streaming loads
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      const int64_t i = base + j * NT + threadIdx.x;
+      ns.dst[j] = i < end ? __ldg(&p.perm[i]) : 0u;
+      ns.x[j] = i < end ? __ldg(&p.xs[i]) : 2.0;
     }
   }
 }
@@ -644,72 +651,94 @@ __device__ __forceinline__ int64_t bin_window_lo(const GatherParams<R>& p, int64
   return lo;
 }
 
-// thread 0 issues the TMA copies of key k's window into buf (expect_tx on bar); all threads zero-fill
-// the parts outside I_L (non-periodic).  Returns false for an empty key (nothing issued).
-template <typename R, int NT>
-__device__ __forceinline__ bool issue_bin_window(const GatherParams<R>& p, int64_t k, int m,
+// Thread 0 only: window of key k into buf -- zero extension outside I_L (reading A5; generic stores
+// published by the expect_tx arrive that follows them) or wrapped copies (Algorithm 1), then the TMA
+// bulk copies completing on bar.
+template <typename R>
+__device__ __forceinline__ void issue_bin_window(const GatherParams<R>& p, int64_t k, int m,
                                                  typename CT<R>::C* buf, uint64_t* bar) {
   using C = typename CT<R>::C;
-  if (__ldg(&p.key_start[k + 1]) == __ldg(&p.key_start[k])) return false;
-  const int64_t bin = k % p.nb[0];
-  const int64_t lo = bin_window_lo(p, bin, m);
+  const int64_t lo = bin_window_lo(p, k % p.nb[0], m);
   const int64_t hi = lo + p.boxcap;
   const int64_t g0 = lo > 0 ? lo : (int64_t)0, g1 = hi < p.L ? hi : p.L;
   const bool periodic = p.wp.alg1 != 0;
-  if (threadIdx.x == 0) {
-    const int64_t wlo = periodic ? (g0 - lo) : 0, whi = periodic ? (hi - g1) : 0;
-    mbar_expect_tx(bar, (uint32_t)((g1 - g0 + wlo + whi) * (int64_t)sizeof(C)));
-    if (g1 > g0) tma_bulk_g2s(buf + (g0 - lo), (const C*)p.grid + g0, (uint32_t)((g1 - g0) * sizeof(C)), bar);
-    if (wlo) tma_bulk_g2s(buf, (const C*)p.grid + (lo + p.L), (uint32_t)(wlo * sizeof(C)), bar);
-    if (whi) tma_bulk_g2s(buf + (g1 - lo), (const C*)p.grid, (uint32_t)(whi * sizeof(C)), bar);
-  }
+  const int64_t wlo = periodic ? (g0 - lo) : 0, whi = periodic ? (hi - g1) : 0;
   if (!periodic) {
-    for (int64_t q = threadIdx.x; q < g0 - lo; q += NT) buf[q] = czero<C>();
-    for (int64_t q = (g1 - lo) + threadIdx.x; q < hi - lo; q += NT) buf[q] = czero<C>();
+    for (int64_t q = 0; q < g0 - lo; ++q) buf[q] = czero<C>();
+    for (int64_t q = g1 - lo; q < hi - lo; ++q) buf[q] = czero<C>();
   }
-  return true;
+  mbar_expect_tx(bar, (uint32_t)((g1 - g0 + wlo + whi) * (int64_t)sizeof(C)));
+  if (g1 > g0) tma_bulk_g2s(buf + (g0 - lo), (const C*)p.grid + g0, (uint32_t)((g1 - g0) * sizeof(C)), bar);
+  if (wlo) tma_bulk_g2s(buf, (const C*)p.grid + (lo + p.L), (uint32_t)(wlo * sizeof(C)), bar);
+  if (whi) tma_bulk_g2s(buf + (g1 - lo), (const C*)p.grid, (uint32_t)(whi * sizeof(C)), bar);
 }
 
 constexpr int kGather1bThreads = 512;
+constexpr int kGather1bBufs = 3;   // window buffers: the issuer needs only the key before last released
 
 template <int T, typename R, bool POLY>
-__global__ void __launch_bounds__(kGather1bThreads) gather1b_kernel(const __grid_constant__ GatherParams<R> p) {
+__global__ void __launch_bounds__(kGather1bThreads, 2) gather1b_kernel(const __grid_constant__ GatherParams<R> p) {
   using C = typename CT<R>::C;
   constexpr int NPT = NPT1<R>::v;
   constexpr int m = T / 2;
   constexpr int NT = kGather1bThreads;
+  constexpr int NB = kGather1bBufs;
   constexpr int64_t CHN = (int64_t)NT * NPT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  C* buf0 = reinterpret_cast<C*>(smem_raw);
-  C* buf1 = buf0 + p.boxcap;
-  __shared__ __align__(8) uint64_t bars[2];
+  C* bufs = reinterpret_cast<C*>(smem_raw);
+  __shared__ __align__(8) uint64_t full[NB], empty[NB];
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], NT);
+    }
     fence_mbar_init();
   }
   __syncthreads();
   C* __restrict__ out = (C*)p.out;
-  const int64_t G = gridDim.x;
-  int64_t k = blockIdx.x;
-  if (k < p.nkeys) issue_bin_window<R, NT>(p, k, m, buf0, &bars[0]);
-  __syncthreads();   // zero-fill of the first window visible
-  uint32_t phases = 0u;
-  for (int it = 0; k < p.nkeys; ++it, k += G) {
-    const int b = it & 1;
-    C* bcur = b ? buf1 : buf0;
-    const int64_t s0 = __ldg(&p.key_start[k]), s1 = __ldg(&p.key_start[k + 1]);
-    NodeSet1<R, NPT> cur, nxt;
-    if (s1 > s0) load_nodes_range<R, NPT, NT>(p, s0, s1, cur);
-    // next key's window into the other buffer (its previous user finished before the barrier that
-    // ended the previous iteration)
-    if (k + G < p.nkeys) issue_bin_window<R, NT>(p, k + G, m, b ? buf0 : buf1, &bars[b ^ 1]);
+  const int64_t G = gridDim.x, k0 = blockIdx.x;
+  auto nonempty = [&](int64_t k) { return __ldg(&p.key_start[k + 1]) > __ldg(&p.key_start[k]); };
+  // prologue: windows of the first NB-1 keys
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < NB - 1; ++t) {
+      const int64_t k = k0 + t * G;
+      if (k < p.nkeys && nonempty(k)) issue_bin_window<R>(p, k, m, bufs + t * p.boxcap, &full[t]);
+    }
+  }
+  int64_t s0 = 0, s1 = 0;
+  NodeSet1<R, NPT> cur, nxt;
+  if (k0 < p.nkeys) {
+    s0 = __ldg(&p.key_start[k0]);
+    s1 = __ldg(&p.key_start[k0 + 1]);
+    load_nodes_range<R, NPT, NT>(p, s0, s1, cur);
+  }
+  uint32_t fph = 0u;   // parity of the next completion of full[b]
+  for (int t = 0; k0 + t * G < p.nkeys; ++t) {
+    const int64_t k = k0 + t * G;
+    const int b = t % NB;
+    // window of key t+NB-1 into the buffer of key t-1 (thread 0 waits until every thread released it)
+    if (threadIdx.x == 0) {
+      const int64_t kn = k + (NB - 1) * G;
+      if (kn < p.nkeys && nonempty(kn)) {
+        const int bn = (t + NB - 1) % NB;
+        if (t >= 1) mbar_wait(&empty[bn], (uint32_t)((t - 1) / NB) & 1u);
+        issue_bin_window<R>(p, kn, m, bufs + bn * p.boxcap, &full[bn]);
+      }
+    }
+    // first chunk of the next key in flight while this key is contracted
+    int64_t s0n = 0, s1n = 0;
+    if (k + G < p.nkeys) {
+      s0n = __ldg(&p.key_start[k + G]);
+      s1n = __ldg(&p.key_start[k + G + 1]);
+      load_nodes_range<R, NPT, NT>(p, s0n, s1n, nxt);
+    }
     if (s1 > s0) {
-      mbar_wait(&bars[b], (phases >> b) & 1u);
-      phases ^= 1u << b;
+      mbar_wait(&full[b], (fph >> b) & 1u);
+      fph ^= 1u << b;
+      const C* bcur = bufs + b * p.boxcap;
       const int64_t lo = bin_window_lo(p, k % p.nb[0], m);
       for (int64_t base = s0; base < s1; base += CHN) {
-        if (base + CHN < s1) load_nodes_range<R, NPT, NT>(p, base + CHN, s1, nxt);
+        if (base > s0) load_nodes_range<R, NPT, NT>(p, base, s1, cur);   // tail chunks (rare)
 #pragma unroll
         for (int j = 0; j < NPT; ++j) {
           int c;
@@ -724,10 +753,12 @@ __global__ void __launch_bounds__(kGather1bThreads) gather1b_kernel(const __grid
           for (int kk = 0; kk < T; ++kk) cmac(acc, w[kk], row[kk]);
           out[cur.dst[j]] = acc;
         }
-        cur = nxt;
       }
     }
-    __syncthreads();   // every thread done with buffer b (and the next window's zero-fill visible)
+    mbar_arrive(&empty[b]);   // this thread is done with buffer b
+    cur = nxt;
+    s0 = s0n;
+    s1 = s1n;
   }
 }
 
