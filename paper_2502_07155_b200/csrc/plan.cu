@@ -302,7 +302,9 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   p->d1_binned = false;
   if (o->d == 1 && o->batch == 1 && !(o->flags & BNFFT_PRECOMPUTE_PSI) && lgL - lg > kMaxDigitBits &&
       !getenv("BNFFT_D1_CHUNKED")) {
-    const int lgb = lgL - kMaxDigitBits;
+    int lgc = 0;   // ceil(log2 L): at most 2^kMaxDigitBits bins even for L not a power of two
+    while (((int64_t)1 << lgc) < L) ++lgc;
+    const int lgb = lgc - kMaxDigitBits;
     const size_t win = (((size_t)1 << lgb) + 2 * (size_t)o->m + 2) * (size_t)p->csize;
     if (win <= ((size_t)40 << 10)) {
       lg = lgb;
