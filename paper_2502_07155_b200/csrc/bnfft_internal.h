@@ -74,6 +74,9 @@ struct bnfft_plan_s {
   bnfft::WinParams wp{};
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t pre_stream = nullptr;   // step 0(a) runs here, overlapping node preprocessing
+  cudaEvent_t ev_fork = nullptr, ev_pre = nullptr;
+  bool pre_pending = false;            // main stream has not yet waited for the last precompute
   bool c128 = false;
   size_t csize = 8;  // bytes per complex
 

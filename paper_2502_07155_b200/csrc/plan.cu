@@ -170,6 +170,12 @@ int bnfft_destroy(bnfft_plan_s* p) {
   cudaSetDevice(p->device);
   if (p->stream) cudaStreamSynchronize(p->stream);
   else cudaDeviceSynchronize();
+  if (p->pre_stream) {
+    cudaStreamSynchronize(p->pre_stream);
+    cudaStreamDestroy(p->pre_stream);
+  }
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_pre) cudaEventDestroy(p->ev_pre);
   if (p->fft_ok) cufftDestroy(p->fft);
   dfree(p->d_gl);
   dfree(p->d_psihat);
@@ -197,15 +203,33 @@ int bnfft_destroy(bnfft_plan_s* p) {
   return BNFFT_OK;
 }
 
+// Step 0(a) is independent of the nodes: it runs on a plan-owned side stream forked from the plan's
+// stream, so a following bnfft_set_nodes overlaps it; execute (the consumer of q) joins it.
 int bnfft_precompute(bnfft_plan_s* p) {
   if (!p) return BNFFT_E_INVALID_ARG;
+  cudaSetDevice(p->device);
+  cudaError_t e = cudaEventRecord(p->ev_fork, p->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->pre_stream, p->ev_fork, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "precompute fork");
+  cudaStream_t main_stream = p->stream;
+  p->stream = p->pre_stream;   // launch_psihat and the stage timer use p->stream
   cudaEvent_t ev;
   timer_begin(p, ST_PSIHAT, &ev);
-  cudaError_t e = launch_psihat(p);
+  e = launch_psihat(p);
+  if (e == cudaSuccess) timer_end(p, ST_PSIHAT, ev);
+  p->stream = main_stream;
   if (e != cudaSuccess) return cuda_fail(e, "psihat kernel");
-  timer_end(p, ST_PSIHAT, ev);
+  if ((e = cudaEventRecord(p->ev_pre, p->pre_stream)) != cudaSuccess) return cuda_fail(e, "precompute join");
+  p->pre_pending = true;
   p->n_psihat++;
   return BNFFT_OK;
+}
+
+// make the plan's stream wait for the last precompute (before anything reads psi^ / q)
+static cudaError_t join_precompute(bnfft_plan_s* p) {
+  if (!p->pre_pending) return cudaSuccess;
+  p->pre_pending = false;
+  return cudaStreamWaitEvent(p->stream, p->ev_pre, 0);
 }
 
 int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
@@ -419,8 +443,12 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     }
     p->device_bytes += (int64_t)ws;
 
+    CK(cudaStreamCreateWithFlags(&p->pre_stream, cudaStreamNonBlocking), "side stream");
+    CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "fork event");
+    CK(cudaEventCreateWithFlags(&p->ev_pre, cudaEventDisableTiming), "join event");
     rc = bnfft_precompute(p);
     if (rc != BNFFT_OK) goto fail;
+    CK(join_precompute(p), "precompute join");
     double fl[2];
     CK(cudaMemcpyAsync(fl, p->d_flat, sizeof(fl), cudaMemcpyDeviceToHost, p->stream), "copy flat");
     CK(cudaStreamSynchronize(p->stream), "plan sync");
@@ -545,6 +573,7 @@ int bnfft_execute(bnfft_plan_s* p, const void* fhat, void* f) {
   if (!fhat || (p->n > 0 && !f)) { set_error("NULL buffer"); return BNFFT_E_INVALID_ARG; }
   cudaSetDevice(p->device);
   cudaError_t e;
+  if ((e = join_precompute(p)) != cudaSuccess) return cuda_fail(e, "precompute join");
   cudaEvent_t ev;
   timer_begin(p, ST_DECONV, &ev);
   if ((e = launch_deconv(p, fhat)) != cudaSuccess) return cuda_fail(e, "deconv kernel");
@@ -699,7 +728,8 @@ int bnfft_reset_timing(bnfft_plan_s* p) {
 int bnfft_get_psihat(const bnfft_plan_s* p, double* host_out) {
   if (!p || !host_out) return BNFFT_E_INVALID_ARG;
   cudaSetDevice(p->device);
-  cudaError_t e = cudaMemcpyAsync(host_out, p->d_psihat, p->opts.M * sizeof(double),
+  cudaError_t e = cudaEventSynchronize(p->ev_pre);   // the last precompute has finished
+  if (e == cudaSuccess) e = cudaMemcpyAsync(host_out, p->d_psihat, p->opts.M * sizeof(double),
                                   cudaMemcpyDeviceToHost, p->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
   return e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "get_psihat");
