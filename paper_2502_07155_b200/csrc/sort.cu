@@ -37,6 +37,26 @@ __device__ __forceinline__ int64_t hist_index(const SegLayout& sl, int64_t tile,
 
 // K1: validate + key.  bad = min over nodes of (index << 4 | code).  Each thread handles a pair of
 // consecutive nodes with 16-byte loads/stores (2*D doubles, 2 keys).
+// The common case in one pass: all coordinates in [-1/2, 1/2) (NaN fails the comparison) and, with
+// STRICT_DOMAIN, inside the closed feasible box; the caller falls back to node_key for the error code.
+template <int D>
+__device__ __forceinline__ bool node_key_fast(const double* xv, const KeyParams& kp, uint32_t& key) {
+  bool ok = true;
+  key = 0;
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    const double v = xv[t];
+    ok &= (v >= -0.5) & (v < 0.5);
+    if (kp.strict) ok &= (v >= kp.box_lo) & (v <= kp.box_hi);
+    const double Lx = __dmul_rn(kp.Lf, v);
+    int c = __double2int_rz(floor(Lx)) + (int)(kp.L >> 1);
+    c = min(c, (int)kp.L - 1);
+    key = key * (uint32_t)kp.nb[t] + ((uint32_t)c >> kp.log2W[t]);
+  }
+  if (!ok) key = 0;
+  return ok;
+}
+
 template <int D>
 __device__ __forceinline__ uint32_t node_key(const double* xv, const KeyParams& kp, int& code) {
   uint32_t key = 0;
@@ -161,11 +181,16 @@ __global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(
           if (t < D || full) xcopy[i * D + t] = xv[jj][t];
       }
     }
-    int c0 = 0, c1 = 0;
-    const uint32_t k0 = node_key<D>(xv[jj], kp, c0);
-    const uint32_t k1 = full ? node_key<D>(xv[jj] + D, kp, c1) : 0u;
-    if (c0) atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)c0);
-    if (c1) atomicMin(bad, ((unsigned long long)(i + 1) << 4) | (unsigned long long)c1);
+    uint32_t k0, k1 = 0u;
+    const bool ok0 = node_key_fast<D>(xv[jj], kp, k0);
+    const bool ok1 = !full || node_key_fast<D>(xv[jj] + D, kp, k1);
+    if (!(ok0 && ok1)) {   // rare: error codes of the offending nodes
+      int c0 = 0, c1 = 0;
+      node_key<D>(xv[jj], kp, c0);
+      if (full) node_key<D>(xv[jj] + D, kp, c1);
+      if (c0) atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)c0);
+      if (c1) atomicMin(bad, ((unsigned long long)(i + 1) << 4) | (unsigned long long)c1);
+    }
     atomicAdd(&cnt[k0 & mask], 1u);
     if (full) atomicAdd(&cnt[k1 & mask], 1u);
     if (keys) {   // null: the one-pass d = 1 scatter recomputes the keys from x
@@ -514,8 +539,9 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix1x_scatter_kernel(
     const int li = wbase + j * 32 + lane;
     if (li < tile_n) {
       sx[li] = xv[j];
-      int code;
-      k[j] = node_key<1>(&xv[j], kp, code) & mask;
+      uint32_t kk;
+      node_key_fast<1>(&xv[j], kp, kk);
+      k[j] = kk & mask;
     } else {
       k[j] = 0u;
     }
