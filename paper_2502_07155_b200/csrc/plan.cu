@@ -357,7 +357,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     if (o->d <= 2 && gbytes_one <= ((int64_t)48 << 20)) {
       int64_t per = (int64_t)o->batch * (int64_t)p->csize;
       int ub = kSortTileLog2;
-      const int64_t target = p->d1_binned ? ((int64_t)8 << 20) : ((int64_t)16 << 20);   // measured (cfg2)
+      const int64_t target = (int64_t)16 << 20;   // measured best for cfg2 (both d = 1 kernels)
       while (ub < 31 && (((int64_t)1 << (ub + 1)) * per) <= target) ++ub;
       if (const char* s = getenv("BNFFT_UB_LOG2")) ub = atoi(s);
       ub = std::max(ub, kSortTileLog2);   // user blocks are whole sort tiles
