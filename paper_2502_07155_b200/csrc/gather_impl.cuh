@@ -82,7 +82,13 @@ __device__ __forceinline__ float phi_r(float tau, const WinParams& w) { return p
 __device__ __forceinline__ double sqrt_r(double v) { return sqrt(v); }
 // complex64 edge factors: MUFU reciprocal square root times v (~2 ulp; taps need ~1e-7 absolute),
 // v >= 0 (v == 0 only for Kronecker nodes, which do not use the factor)
-__device__ __forceinline__ float sqrt_r(float v) { return v * rsqrtf(fmaxf(v, 1e-30f)); }
+__device__ __forceinline__ float sqrt_r(float v) {
+  // v * rsqrt(v) with one MUFU op: the argument is clamped to a normal float, so the approximate,
+  // flush-to-zero form needs no denormal fix-up (error ~1 ulp, below the complex64 tap-fit error)
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(v, 1e-30f)));
+  return v * r;
+}
 template <typename R> __device__ __forceinline__ R pi_r();
 template <> __device__ __forceinline__ double pi_r<double>() { return 3.141592653589793; }
 template <> __device__ __forceinline__ float pi_r<float>() { return 3.14159265f; }
@@ -100,7 +106,8 @@ __device__ __forceinline__ DimState<R> dim_state(double u_d, const GatherParams<
   constexpr int m = T / 2;
   DimState<R> st;
   st.u = (R)u_d;
-  st.x = (R)(2.0 * u_d - 1.0);
+  if constexpr (sizeof(R) == 4) st.x = fmaf(2.0f, st.u, -1.0f);   // complex64: from the rounded u
+  else st.x = (R)(2.0 * u_d - 1.0);
   st.hit = (st.u == R(0)) ? m - 1 : ((st.u == R(1)) ? m : -1);
   if (p.wp.alg1) st.hit = -1;   // Algorithm 1: phi(l/L) is no Kronecker delta
   if (POLY) {

@@ -351,3 +351,21 @@ def test_precompute_psi_unsupported(bn):
         with pytest.raises(bn.BnfftError) as ei:
             bn.Plan(d, 64, 2.0, 4, "sinh", "c64", batch=batch, precompute_psi=True)
         assert ei.value.code == bn.BNFFT_E_UNSUPPORTED
+
+
+def test_precompute_side_stream_join(bn, torch):
+    """Step 0(a) runs on the plan's side stream: a precompute issued right before execute (and a
+    psihat read right after it) must see the finished quadrature (fork/join ordering)."""
+    cfg = synth.CONFIGS[2].scaled(M=1 << 16, m=8, N=200_003)
+    x = torch.from_numpy(synth.make_nodes(cfg, variant=31)).cuda()
+    fh = torch.from_numpy(synth.make_spectrum(cfg, variant=31, prec="c64")).cuda()
+    plan = bn.Plan(1, cfg.M, 2.0, 8, "sinh", "c64")
+    plan.set_nodes(x)
+    ref = plan.execute(fh).clone()
+    ph0 = plan.psihat().copy()
+    for _ in range(3):
+        plan.precompute()
+        assert torch.equal(plan.execute(fh), ref)
+        plan.precompute()
+        assert np.array_equal(plan.psihat(), ph0)
+    plan.close()
