@@ -321,7 +321,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   int lgL = 0;
   while (((int64_t)1 << (lgL + 1)) <= L) ++lgL;
   // d = 1, batch 1, large grids: bins wide enough that the key (bin index) fits one radix digit, when
-  // a bin's window (bin + halo) fits the per-CTA double buffer; the gather then walks whole bins
+  // a bin's window (bin + halo) fits three per CTA (<= 72 KB each); the gather then walks whole bins
   // (gather1b).  Otherwise 128-cell bins and the chunked window kernel.
   p->d1_binned = false;
   if (o->d == 1 && o->batch == 1 && !(o->flags & BNFFT_PRECOMPUTE_PSI) && lgL - lg > kMaxDigitBits &&
@@ -330,7 +330,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     while (((int64_t)1 << lgc) < L) ++lgc;
     const int lgb = lgc - kMaxDigitBits;
     const size_t win = (((size_t)1 << lgb) + 2 * (size_t)o->m + 2) * (size_t)p->csize;
-    if (win <= ((size_t)40 << 10)) {
+    if (win <= ((size_t)(getenv("BNFFT_D1_WINMAX_KB") ? atoi(getenv("BNFFT_D1_WINMAX_KB")) : 72) << 10)) {   // 3 windows per CTA fit 227 KB
       lg = lgb;
       p->d1_binned = true;
     }

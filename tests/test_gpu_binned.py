@@ -37,6 +37,8 @@ def sampled_ref(x, fh, M, sigma, m, window, idx, alg1=False):
 CASES = [  # id, M, sigma, m, window, prec, N, exact, alg1
     ("sinh-c64", 1 << 17, 2.0, 8, "sinh", "c64", 1 << 20, False, False),
     ("gauss-c64", 1 << 17, 2.0, 6, "gauss", "c64", 700_001, False, False),
+    ("sinh-c128", 1 << 17, 2.0, 8, "sinh", "c128", 300_007, False, False),
+    ("gauss-c128-alg1-free", 1 << 16, 2.0, 7, "gauss", "c128", 200_003, False, False),
     ("ckb-exact-c64", 1 << 17, 2.0, 5, "ckb", "c64", 300_007, True, False),
     ("nonpow2-L", 150_000, 2.0, 7, "sinh", "c64", 500_003, False, False),
     ("sigma1.5", 1 << 17, 1.5, 4, "sinh", "c64", 400_009, False, False),
