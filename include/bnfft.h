@@ -158,8 +158,11 @@ typedef struct {
 BNFFT_API int bnfft_plan_create(const bnfft_opts* opts, struct bnfft_plan_s** out);
 
 /* Algorithm 2 step 0(a): psi^_1(k), k in I_M, by quadrature on the device, and the
- * folded deconvolution factors q(k) = (-1)^k / (L psi^_1(k)) (A8, A9).  Stream-ordered,
- * asynchronous; plan_create calls it and checks the result. */
+ * folded deconvolution factors q(k) = (-1)^k / (L psi^_1(k)) (A8, A9).  Asynchronous: the work
+ * runs on a plan-owned side stream forked from the plan's stream (an event recorded on the plan's
+ * stream at the call), so it overlaps a following bnfft_set_nodes; bnfft_execute makes the plan's
+ * stream wait for it, and bnfft_get_psihat waits for it.  plan_create calls it and checks the
+ * result. */
 BNFFT_API int bnfft_precompute(struct bnfft_plan_s* plan);
 
 /* Set the node set.  x_dev: device pointer, n x d float64, row-major, user order; may be freed
