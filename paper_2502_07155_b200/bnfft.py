@@ -14,7 +14,9 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint32, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbnfft.so")
+# BNFFT_LIB_VARIANT=<tag> loads libbnfft_<tag>.so (A/B builds of tuning constants; tools/)
+LIB_PATH = os.path.join(_HERE, "libbnfft.so" if not os.environ.get("BNFFT_LIB_VARIANT")
+                        else f"libbnfft_{os.environ['BNFFT_LIB_VARIANT']}.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2502_07155_b200.build` "
                       "(there is no CPU fallback)")
