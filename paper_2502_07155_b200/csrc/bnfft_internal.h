@@ -132,6 +132,7 @@ struct bnfft_plan_s {
   int gather_box_cap = 0;     // d = 1: staged window capacity (complex elements)
   int64_t gather_grid1 = 0;   // persistent grid size (SMs x resident CTAs)
   int gather_nslice = 1, gather_box_elems = 0, gather_bufstride = 0;
+  int gather_nbuf = 2;
   int gather_tbox[3] = {1, 1, 1};
   bool d1_binned = false;         // d = 1: bins of 2^bin_log2 cells, one radix pass, per-bin gather
   void* d_pre_w = nullptr;        // BNFFT_PRECOMPUTE_PSI: [n][2m] weights of the sorted nodes

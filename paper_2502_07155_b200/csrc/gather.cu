@@ -64,7 +64,10 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   int bt = (int)std::max<size_t>(1, std::min<size_t>((size_t)p->opts.batch, budget / per));
   if (bt > 256) bt = 256;
   const size_t buf_bytes = (per * bt + 127) & ~(size_t)127;
-  const int nbuf = use_coop3(p) ? 1 : 2;     // coop kernel: one box buffer, more CTAs per SM
+  // coop kernel: one box buffer, more CTAs per SM; gatherN: three buffers when they fit 100 KB
+  // (mbarrier-released, see gatherN_kernel), else two
+  const int nbuf = use_coop3(p) ? 1 : (3 * buf_bytes <= ((size_t)100 << 10) ? 3 : 2);
+  p->gather_nbuf = nbuf;
   p->gather_bt = bt;
   p->gather_nslice = (p->opts.batch + bt - 1) / bt;
   p->gather_box_elems = (int)box_elems;
@@ -240,6 +243,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
   gp.nkeys = p->nkeys;
   gp.nslice = p->gather_nslice;
   gp.bufstride = p->gather_bufstride;
+  gp.nbuf = p->gather_nbuf;
   for (int t = 0; t < 3; ++t) gp.tbox[t] = p->gather_tbox[t];
   if (p->opts.d >= 2) {
     gp.box_elems = p->gather_box_elems;

@@ -68,7 +68,8 @@ struct GatherParams {
   int64_t nkeys;
   int tbox[3];            // binned kernel: TMA box extents per dim (dim 0 slowest), innermost padded
   int nslice;             // batch slices per unit (bt spectra each)
-  int bufstride;          // binned kernel: elements between the two staging buffers (128-B aligned)
+  int bufstride;          // binned kernel: elements between the staging buffers (128-B aligned)
+  int nbuf;               // binned kernel: staging buffers (2 or 3), released by mbarrier
   int morton_bits;        // d = 3 cooperative kernel: bits per bin coordinate of the Z-order walk
   int64_t nkeys_morton;   // user blocks x 8^morton_bits
   WinParams wp;
@@ -838,7 +839,7 @@ __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_co
   using C = typename CT<R>::C;
   constexpr int m = T / 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t full[3], empty[3];
   const int BZ = p.tbox[D - 1];                      // innermost (padded) extent
   const int BY = D == 3 ? p.tbox[1] : 1;
   const int box_elems = p.box_elems;                 // per spectrum (with padding)
@@ -847,36 +848,58 @@ __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_co
   const uint32_t bytes = buf_elems * (uint32_t)sizeof(C);
   const int64_t G = gridDim.x;
   const int nsl = p.nslice;
+  const int NB = p.nbuf;
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int q = 0; q < NB; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kGatherThreads);
+    }
     fence_mbar_init();
   }
   __syncthreads();
   C* __restrict__ out = (C*)p.out;
 
-  // the CTA's item sequence: keys u = blockIdx.x + j*G (non-empty ones), slices 0..nsl-1 each
+  // the CTA's item sequence: keys u = blockIdx.x + j*G (non-empty ones), slices 0..nsl-1 each.
+  // Item i uses buffer i % NB; thread 0 issues item i+NB-1 once every thread released item i-1, so
+  // threads that finish an item early move on to the next (already staged) one instead of waiting.
   auto next_key = [&](int64_t u) -> int64_t {
     while (u < p.nkeys && __ldg(&p.key_start[u + 1]) == __ldg(&p.key_start[u])) u += G;
     return u;
   };
+  auto advance = [&](int64_t& u, int& sl) {
+    if (u >= p.nkeys) return;
+    if (++sl == nsl) {
+      sl = 0;
+      u = next_key(u + G);
+    }
+  };
   int64_t u = next_key(blockIdx.x);
   int sl = 0;
   if (u >= p.nkeys) return;
-  if (threadIdx.x == 0) issue_box<D, R>(p, tmap, u, 0, buf0, &bars[0], bytes);
+  // look-ahead items (NB - 1 ahead at most 2)
+  int64_t u1 = u, u2;
+  int s1 = sl, s2;
+  advance(u1, s1);
+  u2 = u1;
+  s2 = s1;
+  advance(u2, s2);
+  if (threadIdx.x == 0) {
+    issue_box<D, R>(p, tmap, u, sl, buf0, &full[0], bytes);
+    if (NB == 3 && u1 < p.nkeys) issue_box<D, R>(p, tmap, u1, s1, buf0 + p.bufstride, &full[1], bytes);
+  }
   uint32_t phases = 0u;
   for (int it = 0;; ++it) {
-    const int b = it & 1;
-    // next item
-    int64_t un = u;
-    int sn = sl + 1;
-    if (sn == nsl) {
-      sn = 0;
-      un = next_key(u + G);
+    const int b = it % NB;
+    if (threadIdx.x == 0) {
+      const int64_t ua = NB == 3 ? u2 : u1;
+      const int sa = NB == 3 ? s2 : s1;
+      if (ua < p.nkeys) {
+        const int bn = (it + NB - 1) % NB;
+        if (it >= 1 && NB == 3) mbar_wait(&empty[bn], (uint32_t)((it - 1) / NB) & 1u);
+        issue_box<D, R>(p, tmap, ua, sa, buf0 + bn * p.bufstride, &full[bn], bytes);
+      }
     }
-    if (un < p.nkeys && threadIdx.x == 0)
-      issue_box<D, R>(p, tmap, un, sn, buf0 + (b ^ 1) * p.bufstride, &bars[b ^ 1], bytes);
-    mbar_wait(&bars[b], (phases >> b) & 1u);
+    mbar_wait(&full[b], (phases >> b) & 1u);
     phases ^= 1u << b;
     const C* box = buf0 + b * p.bufstride;
     // bin origin (cells) of key u
@@ -944,10 +967,16 @@ __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_co
         out[(int64_t)(sl * p.bt + bb) * p.n + dst] = acc;
       }
     }
-    if (un >= p.nkeys) break;
-    __syncthreads();   // everyone done with buffer b before it is refilled (item after next)
-    u = un;
-    sl = sn;
+    if (u1 >= p.nkeys) break;
+    // buffer b is refilled NB-1 items later: three buffers hand it back per thread (mbarrier), two
+    // (large batched boxes) with a CTA barrier, which measured faster there (cfg5)
+    if (NB == 3) mbar_arrive(&empty[b]);
+    else __syncthreads();
+    u = u1;
+    sl = s1;
+    u1 = u2;
+    s1 = s2;
+    advance(u2, s2);
   }
 }
 
