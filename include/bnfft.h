@@ -61,7 +61,9 @@ typedef enum {
   BNFFT_E_CUFFT = -12,                   /* cuFFT error                                      */
   BNFFT_E_OOM = -13,                     /* device allocation failed                         */
   BNFFT_E_UNSUPPORTED = -14,             /* parameters outside the compiled kernel set       */
-  BNFFT_E_INVALID_ARG = -15              /* NULL plan/pointer, n < 0, n >= 2^31, ...         */
+  BNFFT_E_INVALID_ARG = -15,             /* NULL plan/pointer, n < 0, n >= 2^31, ...         */
+  BNFFT_E_NCCL = -16                     /* NCCL (or local-group transport) error, or the NCCL
+                                            library could not be loaded                      */
 } bnfft_status;
 
 typedef enum { BNFFT_SINH = 0, BNFFT_GAUSS = 1, BNFFT_CKB = 2 } bnfft_window;
@@ -75,11 +77,33 @@ enum {
                                 periodic short sums with the window phi (no sinc); nodes on the
                                 torus [-1/2,1/2)^d.  d = 1; sinh / cKB windows; default shape
                                 beta = 2 pi m (1 - 1/(2 sigma)) (reading A17)               */,
-  BNFFT_PRECOMPUTE_PSI = 64u /* Algorithm 2 step 0(b): set_nodes evaluates the kernel at every
+  BNFFT_PRECOMPUTE_PSI = 64u,/* Algorithm 2 step 0(b): set_nodes evaluates the kernel at every
                                 (node, tap) once and stores it (2m values per node); execute reads
                                 them instead of evaluating the tap polynomials.  d = 1, batch 1.
                                 Costs 2m * (4|8) bytes per node of device memory.              */
+  BNFFT_SORTED_OUTPUT = 128u,/* execute writes f in the plan's sorted node order (f_dev[i] is the value
+                                of user node perm[i], bnfft_get_perm) instead of user order: the
+                                gather's stores become sequential.  Single rank only.            */
+  BNFFT_BALANCED_SLABS = 256u/* BNFFT_DIST_SLAB: slab cut points chosen from the all-reduced per-plane
+                                node histogram (equal node counts) instead of equal plane counts */
 };
+
+/* Multi-GPU modes (bnfft_opts.dist; nranks > 1).  Step 3 is independent per node once theta exists
+ * (P:510-513), so ranks exchange only grid planes and node records:
+ *   BNFFT_DIST_REPLICATE  every rank computes the whole theta grid and evaluates its own nodes; no
+ *                         communication (results bitwise equal to one GPU).
+ *   BNFFT_DIST_SLAB       d = 3: rank r owns the theta planes l_2 in [a_r, b_r) (slab along the
+ *                         second dimension).  Step 2 is a distributed slab FFT (per-rank 2-D FFTs over
+ *                         (k_2, k_3) of its k_1 chunk, an all-to-all, 1-D FFTs along k_1), the m-halo
+ *                         planes [a_r - m + 1, a_r) and [b_r, b_r + m) are exchanged with the
+ *                         neighbours (zero beyond the global ends: Psi is not periodic),
+ *                         set_nodes sends every node to the rank owning its cell and execute returns
+ *                         the values to the originating rank, in its user order.
+ * Transport: an NCCL communicator (nccl_comm = ncclComm_t, e.g. torch's ProcessGroupNCCL comm or
+ * bnfft_nccl_comm_init) with one process per GPU, or a local group (local_group =
+ * bnfft_group_create(nranks)) of nranks plans driven by nranks host threads of one process, on any
+ * device(s) -- the same exchange code over cudaMemcpyAsync, for tests on one GPU. */
+enum { BNFFT_DIST_REPLICATE = 0, BNFFT_DIST_SLAB = 1 };
 
 /* Plan options.  d: 1..3.  M: even >= 2.  sigma >= 1, L = 2 ceil(ceil(sigma M)/2).
  * m: truncation parameter, 1 <= m, 2m < L; compiled range m <= 16 (d=1), 12 (d=2), 8 (d=3).
@@ -100,6 +124,11 @@ typedef struct {
   uint32_t flags;
   int32_t device;
   void* stream;
+  /* multi-GPU (all zero / NULL = one GPU) */
+  int32_t rank, nranks;   /* this plan's rank in [0, nranks); nranks <= 1: single GPU            */
+  void* nccl_comm;        /* ncclComm_t of nranks ranks (this plan's rank = its NCCL rank), or NULL */
+  void* local_group;      /* bnfft_group handle (in-process transport), or NULL                   */
+  int32_t dist;           /* BNFFT_DIST_REPLICATE or BNFFT_DIST_SLAB                              */
 } bnfft_opts;
 
 /* Plan description.  Node binning geometry (for the stable bin sort, row a1): the cell of
@@ -132,6 +161,10 @@ typedef struct {
   int64_t grid_bytes;       /* bytes of one theta grid (batch x L^d complex)               */
   int64_t device_bytes;     /* device memory currently owned by the plan                   */
   int32_t gather_kernel;    /* step-3 kernel execute launches: BNFFT_GK_*                  */
+  int32_t rank, nranks, dist;
+  int64_t slab_lo, slab_hi; /* DIST_SLAB: this rank's planes [slab_lo, slab_hi) of dimension 2 */
+  int64_t n_owned;          /* DIST_SLAB: nodes this rank evaluates (its slab's nodes)      */
+  int64_t halo_bytes;       /* DIST_SLAB: grid bytes received from the neighbours per execute */
 } bnfft_info;
 
 /* bnfft_info.gather_kernel */
@@ -141,7 +174,8 @@ enum {
   BNFFT_GK_SEGMENT = 2,   /* d = 1 batched: generic segment kernel (gather_kernel)          */
   BNFFT_GK_BOX = 3,       /* d = 2, 3: binned TMA-box kernel (gatherN_kernel)               */
   BNFFT_GK_COOP3 = 4,     /* d = 3, m = 4, complex64: warp-cooperative kernel (gather3c)    */
-  BNFFT_GK_PRE1 = 5       /* d = 1 with BNFFT_PRECOMPUTE_PSI (gather1_kernel, stored taps)  */
+  BNFFT_GK_PRE1 = 5,      /* d = 1 with BNFFT_PRECOMPUTE_PSI (gather1_kernel, stored taps)  */
+  BNFFT_GK_SWEEP3 = 6     /* d = 3, m = 4, complex64: z-sweep kernel (gather3s_kernel)       */
 };
 
 /* Per-stage device times (ms) accumulated since the last reset, and call counts.  Only
@@ -151,6 +185,7 @@ typedef struct {
   double ms_psihat, ms_keys, ms_sort, ms_build, ms_deconv, ms_fft, ms_gather;
   int64_t n_psihat, n_set_nodes, n_execute;
   int64_t kernel_launches;  /* this library's own kernels launched (cuFFT not counted)    */
+  double ms_exchange;       /* multi-GPU: node exchange, FFT all-to-all, halos, output return */
 } bnfft_timing;
 
 /* Create a plan: validates options, allocates device buffers, creates the cuFFT plan and runs
@@ -216,6 +251,51 @@ BNFFT_API int bnfft_get_bin_offsets(struct bnfft_plan_s* plan, uint32_t* dev_out
 
 /* Release every resource of the plan (after synchronizing its stream).  NULL is a no-op. */
 BNFFT_API int bnfft_destroy(struct bnfft_plan_s* plan);
+
+/* ---- multi-GPU transport (see BNFFT_DIST_*) ----
+ * bnfft_nccl_unique_id: 128 bytes (ncclUniqueId) into out128, to be broadcast to every rank.
+ * bnfft_nccl_comm_init: ncclCommInitRank on `device`; *comm_out is an ncclComm_t for bnfft_opts.
+ * bnfft_nccl_comm_destroy: ncclCommDestroy.  NCCL is loaded at run time (libnccl.so.2, the copy
+ * already in the process if any); without it these return BNFFT_E_NCCL.
+ * bnfft_group_create / destroy: an in-process group of nranks ranks; each rank's plan is created
+ * and driven by its own host thread (collective calls block until every rank has arrived). */
+BNFFT_API int bnfft_nccl_unique_id(void* out128);
+BNFFT_API int bnfft_nccl_comm_init(const void* id128, int32_t nranks, int32_t rank, int32_t device, void** comm_out);
+BNFFT_API int bnfft_nccl_comm_destroy(void* comm);
+BNFFT_API int bnfft_group_create(int32_t nranks, void** group_out);
+BNFFT_API int bnfft_group_destroy(void* group);
+
+/* Host-side partition logic of BNFFT_DIST_SLAB (pure functions, no device):
+ * bnfft_slab_cuts: cut points cuts[0..nranks] (cuts[0] = 0, cuts[nranks] = L, multiples of `align`)
+ *   of L planes; plane_counts == NULL gives equal plane counts, else (K10) the cuts that balance the
+ *   cumulative node counts plane_counts[0..L) (each rank >= align planes when L allows).
+ * bnfft_slab_owner: rank owning plane c (cuts as above).
+ * bnfft_halo_ranges: for rank r, the planes it receives: [lo_from, a_r) from rank r-1 and
+ *   [b_r, hi_from) from rank r+1, clipped to [0, L) (lower = m-1 planes, upper = m planes). */
+BNFFT_API int bnfft_slab_cuts(const int64_t* plane_counts, int64_t L, int32_t nranks, int32_t align, int64_t* cuts);
+BNFFT_API int32_t bnfft_slab_owner(const int64_t* cuts, int32_t nranks, int64_t c);
+BNFFT_API int bnfft_halo_ranges(const int64_t* cuts, int32_t nranks, int32_t rank, int32_t m, int64_t L,
+                                int64_t* below_lo, int64_t* above_hi);
+
+/* Pipe-throughput microbenchmarks (the FP32 / FP64 / MUFU / shared-memory peaks the
+ * gather kernels are measured against).  One full wave of independent dependency chains per
+ * pipe; *_per_sm_clk = operations (bytes for LDS) per SM per SM cycle (clock64 inside the CTAs),
+ * *_per_s = per second for the whole GPU (CUDA events), *_mhz = the SM clock that implies.
+ * ffma: 3-register FFMA, counted in FMAs; ffma2: fma.rn.f32x2, counted in FMAs (2 per lane);
+ * dfma: FP64 FMAs; ex2 / rsqrt / rcp: MUFU ops (approx.ftz); lds64 / lds128: bytes of
+ * conflict-free 8- / 16-byte shared loads.  Synchronous; takes ~1 s on a B200. */
+typedef struct {
+  int32_t sms;
+  double ffma_per_sm_clk, ffma_per_s, ffma_mhz;
+  double ffma2_per_sm_clk, ffma2_per_s, ffma2_mhz;
+  double dfma_per_sm_clk, dfma_per_s, dfma_mhz;
+  double ex2_per_sm_clk, ex2_per_s, ex2_mhz;
+  double rsqrt_per_sm_clk, rsqrt_per_s, rsqrt_mhz;
+  double rcp_per_sm_clk, rcp_per_s, rcp_mhz;
+  double lds64_per_sm_clk, lds64_per_s, lds64_mhz;
+  double lds128_per_sm_clk, lds128_per_s, lds128_mhz;
+} bnfft_peaks;
+BNFFT_API int bnfft_measure_peaks(int32_t device, bnfft_peaks* out);
 
 BNFFT_API const char* bnfft_status_string(int status);
 BNFFT_API const char* bnfft_last_error(void);

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/bnfft.h"
@@ -63,7 +64,9 @@ struct Timer {
   cudaEvent_t a, b;
 };
 
-enum Stage { ST_PSIHAT = 0, ST_KEYS, ST_SORT, ST_BUILD, ST_DECONV, ST_FFT, ST_GATHER, ST_COUNT };
+enum Stage { ST_PSIHAT = 0, ST_KEYS, ST_SORT, ST_BUILD, ST_DECONV, ST_FFT, ST_GATHER, ST_EXCH, ST_COUNT };
+
+struct DistState;   // multi-GPU state of a plan (dist.cu)
 
 }  // namespace bnfft
 
@@ -133,6 +136,7 @@ struct bnfft_plan_s {
   int64_t gather_grid1 = 0;   // persistent grid size (SMs x resident CTAs)
   int gather_nslice = 1, gather_box_elems = 0, gather_bufstride = 0;
   int gather_nbuf = 2;
+  int gather_threads = 256;      // threads per CTA of the d >= 2 gather launch
   int gather_tbox[3] = {1, 1, 1};
   bool d1_binned = false;         // d = 1: bins of 2^bin_log2 cells, one radix pass, per-bin gather
   void* d_pre_w = nullptr;        // BNFFT_PRECOMPUTE_PSI: [n][2m] weights of the sorted nodes
@@ -147,6 +151,10 @@ struct bnfft_plan_s {
   double ms[bnfft::ST_COUNT] = {0};
   int64_t n_psihat = 0, n_set = 0, n_exec = 0, launches = 0;
   int64_t device_bytes = 0;
+  std::vector<std::pair<void*, size_t>> allocs;   // live plan allocations (device_bytes accounting)
+
+  // multi-GPU (nranks > 1): transport, slab geometry, node exchange (dist.cu)
+  bnfft::DistState* dist = nullptr;
 };
 
 namespace bnfft {
@@ -174,5 +182,16 @@ size_t gather_box_elems(const bnfft_plan_s* p);
 cudaError_t gather_prepare(bnfft_plan_s* p);
 cudaError_t launch_prepsi(bnfft_plan_s* p);
 int tap_coef_count(bool c128);
+cudaError_t dmalloc_bytes(bnfft_plan_s* p, void** ptr, size_t bytes);   // plan-owned, counted
+void dfree_plan(bnfft_plan_s* p, void* ptr);
+
+// multi-GPU (dist.cu); nranks > 1 plans route set_nodes / execute through these
+int dist_create(bnfft_plan_s* p);                 // plan_create: transport + slab geometry + FFT plans
+void dist_destroy(bnfft_plan_s* p);
+int dist_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad);
+int dist_execute(bnfft_plan_s* p, const void* fhat, void* f);
+void dist_fill_info(const bnfft_plan_s* p, bnfft_info* o);
+int local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad);   // single-rank body
+cudaError_t launch_deconv_slab(bnfft_plan_s* p, const void* fhat, void* out, int64_t k0_lo, int64_t k0_hi);
 
 }  // namespace bnfft

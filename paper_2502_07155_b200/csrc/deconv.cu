@@ -54,3 +54,44 @@ cudaError_t launch_deconv(bnfft_plan_s* p, const void* fhat) {
 }
 
 }  // namespace bnfft
+
+namespace bnfft {
+
+// BNFFT_DIST_SLAB step 1 for one rank's k_1 chunk [k0_lo, k0_hi) (d = 3, batch 1): the same products
+// as deconv_kernel, written to out[k_1 - k0_lo][k_2 mod L][k_3 mod L] (the input of the rank's 2-D
+// FFTs over (k_2, k_3)); entries outside I_M stay zero from plan creation.
+template <typename C, typename R>
+__global__ void deconv_slab_kernel(const C* __restrict__ fhat, C* __restrict__ X, const double* __restrict__ q,
+                                   int64_t M, int64_t L, int64_t k0_lo, int64_t total) {
+  const int64_t MM = M * M;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = idx / MM;                 // chunk-local k_1 index
+    const int64_t r = idx - i0 * MM;
+    const int64_t i1 = r / M, i2 = r - (r / M) * M;
+    const int64_t c0 = k0_lo + M / 2 + i0;       // centred index of k_1
+    const int64_t k1 = i1 - M / 2, k2 = i2 - M / 2;
+    const double qq = q[c0] * q[i1] * q[i2];
+    C v = fhat[c0 * MM + r];
+    const R s = (R)qq;
+    v.x *= s;
+    v.y *= s;
+    X[(i0 * L + (k1 < 0 ? k1 + L : k1)) * L + (k2 < 0 ? k2 + L : k2)] = v;
+  }
+}
+
+cudaError_t launch_deconv_slab(bnfft_plan_s* p, const void* fhat, void* out, int64_t k0_lo, int64_t k0_hi) {
+  const int64_t total = (k0_hi - k0_lo) * p->opts.M * p->opts.M;
+  if (total <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148LL * 32);
+  if (p->c128)
+    deconv_slab_kernel<double2, double><<<(unsigned)blocks, 256, 0, p->stream>>>(
+        (const double2*)fhat, (double2*)out, p->d_q, p->opts.M, p->L, k0_lo, total);
+  else
+    deconv_slab_kernel<float2, float><<<(unsigned)blocks, 256, 0, p->stream>>>(
+        (const float2*)fhat, (float2*)out, p->d_q, p->opts.M, p->L, k0_lo, total);
+  p->launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace bnfft

@@ -9,17 +9,25 @@ namespace bnfft {
 
 const void* gather3c_kernel_p();
 const void* gather3c_kernel_e();
+const void* gather3s_kernel_ptr(bool poly);
+size_t gather3s_smem();
+int gather3s_threads();
+int gather3s_row_stride();
 
-// d = 3, m = 4, complex64: the warp-cooperative kernel (conflict-free shared-memory layout)
+// d = 3, m = 4, complex64, batch 1: bins of 8 x 8 x 16 cells and a specialised kernel -- the half-warp
+// kernel gather3c by default; the z-sweep kernel (gather3s.cu) with BNFFT_GATHER3S set at plan
+// creation (measured slower on cfg4: DESIGN.md §8)
 static bool use_coop3(const bnfft_plan_s* p) {
   return p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
 }
+static bool use_sweep3(const bnfft_plan_s* p) { return use_coop3(p) && getenv("BNFFT_GATHER3S"); }
 
 static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false, bool pre = false,
                                 bool binned = false) {
   if (d == 1 && pre && !batched) return c128 ? gather_kernel_1d(m + 300, poly) : gather_kernel_1f(m + 300, poly);
   if (d == 1 && binned && !batched) return c128 ? gather_kernel_1d(m + 400, poly) : gather_kernel_1f(m + 400, poly);
-  if (d == 3 && m == 4 && !c128 && !batched) return poly ? gather3c_kernel_p() : gather3c_kernel_e();
+  if (d == 3 && m == 4 && !c128 && !batched)
+    return getenv("BNFFT_GATHER3S") ? gather3s_kernel_ptr(poly) : (poly ? gather3c_kernel_p() : gather3c_kernel_e());
   if (d == 1 && batched) return c128 ? gather_kernel_1d(m + 100, poly) : gather_kernel_1f(m + 100, poly);
   if (d == 1) return c128 ? gather_kernel_1d(m, poly) : gather_kernel_1f(m, poly);
   if (d == 2) return c128 ? gather_kernel_2d(m, poly) : gather_kernel_2f(m, poly);
@@ -56,7 +64,7 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   int ext[3];
   for (int t = 0; t < d; ++t) ext[t] = (1 << p->bin_log2[t]) + T - 1;
   if (!p->c128) ext[d - 1] = (1 << p->bin_log2[d - 1]) + T;   // even start shift + 16-B multiple
-  if (use_coop3(p)) ext[d - 1] = kRow3;                       // conflict-free rows (bins 8x8x16)
+  if (use_coop3(p)) ext[d - 1] = use_sweep3(p) ? gather3s_row_stride() : kRow3;   // conflict-free rows
   size_t box_elems = 1;
   for (int t = 0; t < d; ++t) box_elems *= (size_t)ext[t];
   const size_t per = box_elems * p->csize;
@@ -73,13 +81,14 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   p->gather_box_elems = (int)box_elems;
   p->gather_bufstride = (int)(buf_bytes / p->csize);
   for (int t = 0; t < 3; ++t) p->gather_tbox[t] = t < d ? ext[t] : 1;
-  p->gather_smem = nbuf * buf_bytes;
+  p->gather_smem = use_sweep3(p) ? gather3s_smem() : nbuf * buf_bytes;
+  p->gather_threads = use_sweep3(p) ? gather3s_threads() : kGatherThreads;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0, nsm = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGatherThreads, p->gather_smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->gather_threads, p->gather_smem);
   if (e != cudaSuccess) return e;
   p->gather_grid1 = (int64_t)std::max(1, per_sm) * nsm;
 
@@ -222,6 +231,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
   gp.boxcap = p->gather_box_cap;
   gp.xs_user = p->xs_user ? 1 : 0;
   gp.pre_w = (R*)p->d_pre_w;
+  gp.sorted_out = (p->opts.flags & BNFFT_SORTED_OUTPUT) ? 1 : 0;
   constexpr int NC = PolyN<R>::NC;
   constexpr int NH = PolyH<R>::NH;
   static_assert(2 * NH == NC, "even/odd split of the tap polynomials");
@@ -256,7 +266,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
     }
     void* args2[] = {&gp, &p->d_tmap};
     unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p->gather_grid1, p->nkeys));
-    cudaError_t e2 = cudaLaunchKernel(fn, dim3(nb), dim3(kGatherThreads), args2, p->gather_smem, p->stream);
+    cudaError_t e2 = cudaLaunchKernel(fn, dim3(nb), dim3(p->gather_threads), args2, p->gather_smem, p->stream);
     p->launches++;
     return e2;
   }
@@ -283,6 +293,10 @@ cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
   if (p->n == 0) return cudaSuccess;
   const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1,
                                  (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0, p->d1_binned);
+  // d = 3, m = 4, complex64: the kernel chosen at plan creation (its launch shape is in the plan)
+  if (use_coop3(p))
+    fn = p->gather_threads == gather3s_threads() ? gather3s_kernel_ptr(p->tap_poly)
+                                                 : (p->tap_poly ? gather3c_kernel_p() : gather3c_kernel_e());
   if (!fn) return cudaErrorInvalidValue;
   return p->c128 ? launch_gather_t<double>(p, out, fn) : launch_gather_t<float>(p, out, fn);
 }

@@ -72,6 +72,7 @@ struct GatherParams {
   int nbuf;               // binned kernel: staging buffers (2 or 3), released by mbarrier
   int morton_bits;        // d = 3 cooperative kernel: bits per bin coordinate of the Z-order walk
   int64_t nkeys_morton;   // user blocks x 8^morton_bits
+  int sorted_out;         // BNFFT_SORTED_OUTPUT: f written at the sorted position i, not at perm[i]
   WinParams wp;
   alignas(16) R ceo[PolyH<R>::NH][kMaxTaps / 2][2];   // [k][i][0] = E_i coeff k, [k][i][1] = O_i
 };
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const __grid_con
           C res;
           res.x = ax;
           res.y = ay;
-          out[(int64_t)(b0 + bb) * p.n + dst] = res;
+          out[(int64_t)(b0 + bb) * p.n + (p.sorted_out ? i : (int64_t)dst)] = res;
         }
       }
     }
@@ -617,7 +618,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather1_kernel(const __grid_co
           if (pos >= 0 && pos < p.L) cmac(acc, w[kk], __ldg(&grid[pos]));
         }
       }
-      out[cur.dst[j]] = acc;
+      out[p.sorted_out ? k * (int64_t)kGatherThreads * NPT + j * kGatherThreads + threadIdx.x : (int64_t)cur.dst[j]] = acc;
     }
     cur = nxt;
     nxt = nn;
@@ -759,7 +760,7 @@ __global__ void __launch_bounds__(kGather1bThreads, 2) gather1b_kernel(const __g
           const C* row = bcur + (c - (m - 1) - lo);
 #pragma unroll
           for (int kk = 0; kk < T; ++kk) cmac(acc, w[kk], row[kk]);
-          out[cur.dst[j]] = acc;
+          out[p.sorted_out ? base + j * NT + threadIdx.x : (int64_t)cur.dst[j]] = acc;
         }
       }
     }
@@ -964,7 +965,7 @@ __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_co
             cmac(acc, wa, pacc);
           }
         }
-        out[(int64_t)(sl * p.bt + bb) * p.n + dst] = acc;
+        out[(int64_t)(sl * p.bt + bb) * p.n + (p.sorted_out ? i : (int64_t)dst)] = acc;
       }
     }
     if (u1 >= p.nkeys) break;
@@ -1086,7 +1087,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather3c_kernel(const __grid_c
             sw[1] = make_float4(w[4], w[5], w[6], w[7]);
           }
         }
-        s_od[wid][lane] = make_int4(od[0], od[1], od[2], (int)dst);
+        s_od[wid][lane] = make_int4(od[0], od[1], od[2], p.sorted_out ? (int)i : (int)dst);
       }
       __syncwarp();
       if (!waited) {

@@ -95,16 +95,32 @@ static int ceil_log2(int64_t v) {
   return b;
 }
 
-template <typename T>
-static cudaError_t dmalloc(bnfft_plan_s* p, T** ptr, size_t bytes) {
+// plan-owned device allocations, counted in bnfft_info.device_bytes while they are live
+cudaError_t dmalloc_bytes(bnfft_plan_s* p, void** ptr, size_t bytes) {
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc((void**)ptr, bytes);
-  if (e == cudaSuccess) p->device_bytes += (int64_t)bytes;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaSuccess) {
+    p->device_bytes += (int64_t)bytes;
+    p->allocs.emplace_back(*ptr, bytes);
+  }
   return e;
 }
 
-static void dfree(void* ptr) {
-  if (ptr) cudaFree(ptr);
+void dfree_plan(bnfft_plan_s* p, void* ptr) {
+  if (!ptr) return;
+  for (size_t i = 0; i < p->allocs.size(); ++i)
+    if (p->allocs[i].first == ptr) {
+      p->device_bytes -= (int64_t)p->allocs[i].second;
+      p->allocs[i] = p->allocs.back();
+      p->allocs.pop_back();
+      break;
+    }
+  cudaFree(ptr);
+}
+
+template <typename T>
+static cudaError_t dmalloc(bnfft_plan_s* p, T** ptr, size_t bytes) {
+  return dmalloc_bytes(p, (void**)ptr, bytes);
 }
 
 static int collect_timing(bnfft_plan_s* p) {
@@ -122,11 +138,11 @@ static int collect_timing(bnfft_plan_s* p) {
 }
 
 static void free_nodes(bnfft_plan_s* p) {
-  dfree(p->d_xs);
-  dfree(p->d_k0);
-  dfree(p->d_k1);
-  dfree(p->d_v0);
-  dfree(p->d_v1);
+  dfree_plan(p, p->d_xs);
+  dfree_plan(p, p->d_k0);
+  dfree_plan(p, p->d_k1);
+  dfree_plan(p, p->d_v0);
+  dfree_plan(p, p->d_v1);
   p->d_xs = nullptr;
   p->d_k0 = p->d_k1 = p->d_v0 = p->d_v1 = nullptr;
   p->d_perm = p->d_skeys = nullptr;
@@ -155,6 +171,7 @@ const char* bnfft_status_string(int s) {
     case BNFFT_E_OOM: return "out of device memory";
     case BNFFT_E_UNSUPPORTED: return "unsupported parameters";
     case BNFFT_E_INVALID_ARG: return "invalid argument";
+    case BNFFT_E_NCCL: return "NCCL / multi-GPU transport error";
     default: return "unknown status";
   }
 }
@@ -177,22 +194,24 @@ int bnfft_destroy(bnfft_plan_s* p) {
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_pre) cudaEventDestroy(p->ev_pre);
   if (p->fft_ok) cufftDestroy(p->fft);
-  dfree(p->d_gl);
-  dfree(p->d_psihat);
-  dfree(p->d_q);
-  dfree(p->d_flat);
-  dfree(p->d_fft_in);
-  dfree(p->d_grid);
-  dfree(p->d_bin_start);
-  dfree(p->d_hist);
-  dfree(p->d_scan_part);
-  dfree(p->d_bad);
-  dfree(p->d_x_stage);
-  dfree(p->d_fhat_stage);
-  dfree(p->d_f_stage);
-  dfree(p->d_tmap);
-  dfree(p->d_pre_w);
+  dist_destroy(p);
+  dfree_plan(p, p->d_gl);
+  dfree_plan(p, p->d_psihat);
+  dfree_plan(p, p->d_q);
+  dfree_plan(p, p->d_flat);
+  dfree_plan(p, p->d_fft_in);
+  dfree_plan(p, p->d_grid);
+  dfree_plan(p, p->d_bin_start);
+  dfree_plan(p, p->d_hist);
+  dfree_plan(p, p->d_scan_part);
+  dfree_plan(p, p->d_bad);
+  dfree_plan(p, p->d_x_stage);
+  dfree_plan(p, p->d_fhat_stage);
+  dfree_plan(p, p->d_f_stage);
+  dfree_plan(p, p->d_tmap);
+  dfree_plan(p, p->d_pre_w);
   free_nodes(p);
+  for (auto& a : p->allocs) cudaFree(a.first);   // anything a partially built plan still owns
   if (p->h_bad) cudaFreeHost(p->h_bad);
   for (auto& t : p->pending) {
     cudaEventDestroy(t.a);
@@ -249,6 +268,8 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   }
   if (o->prec != BNFFT_C64 && o->prec != BNFFT_C128) { set_error("prec"); return BNFFT_E_INVALID_ARG; }
   if (o->batch < 1) { set_error("batch >= 1"); return BNFFT_E_INVALID_ARG; }
+  if (o->nranks > 1 && (o->rank < 0 || o->rank >= o->nranks)) { set_error("rank in [0, nranks)"); return BNFFT_E_INVALID_ARG; }
+  const bool slab = o->nranks > 1 && o->dist == BNFFT_DIST_SLAB;
   if (!gather_supported(o->d, o->m)) { set_error("m outside the compiled range for this d"); return BNFFT_E_UNSUPPORTED; }
   const bool alg1 = (o->flags & BNFFT_ALG1) != 0;
   if ((o->flags & BNFFT_PRECOMPUTE_PSI) && (o->d != 1 || o->batch != 1)) {
@@ -386,11 +407,13 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     CK(dmalloc(p, &p->d_q, o->M * sizeof(double)), "alloc q");
     CK(dmalloc(p, &p->d_flat, 2 * sizeof(double)), "alloc flat");
     size_t gbytes = (size_t)Ld * o->batch * p->csize;
-    CK(dmalloc(p, &p->d_fft_in, gbytes), "alloc fft input");
+    // BNFFT_DIST_SLAB: the grid is indexed globally but only the rank's slab and halos are written;
+    // step 2 runs on the slab buffers of dist.cu (no whole-grid FFT input or plan)
+    if (!slab) CK(dmalloc(p, &p->d_fft_in, gbytes), "alloc fft input");
     CK(dmalloc(p, &p->d_grid, gbytes), "alloc grid");
     CK(dmalloc(p, &p->d_bad, sizeof(unsigned long long)), "alloc status");
     CK(cudaMallocHost((void**)&p->h_bad, sizeof(unsigned long long)), "alloc pinned status");
-    CK(cudaMemsetAsync(p->d_fft_in, 0, gbytes, p->stream), "zero fft input");
+    if (!slab) CK(cudaMemsetAsync(p->d_fft_in, 0, gbytes, p->stream), "zero fft input");
     CK(cudaMemsetAsync(p->d_grid, 0, gbytes, p->stream), "zero grid");
     double th[2 * kQuadN];
     gauss_legendre_theta(kQuadN, th, th + kQuadN);
@@ -427,13 +450,16 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
 
     int n[3] = {(int)L, (int)L, (int)L};
     size_t ws = 0;
-    cufftResult fr = cufftCreate(&p->fft);
-    if (fr == CUFFT_SUCCESS) {
-      p->fft_ok = true;
-      fr = cufftMakePlanMany(p->fft, o->d, n, nullptr, 1, (int)Ld, nullptr, 1, (int)Ld,
-                             p->c128 ? CUFFT_Z2Z : CUFFT_C2C, o->batch, &ws);
+    cufftResult fr = CUFFT_SUCCESS;
+    if (!slab) {
+      fr = cufftCreate(&p->fft);
+      if (fr == CUFFT_SUCCESS) {
+        p->fft_ok = true;
+        fr = cufftMakePlanMany(p->fft, o->d, n, nullptr, 1, (int)Ld, nullptr, 1, (int)Ld,
+                               p->c128 ? CUFFT_Z2Z : CUFFT_C2C, o->batch, &ws);
+      }
+      if (fr == CUFFT_SUCCESS) fr = cufftSetStream(p->fft, p->stream);
     }
-    if (fr == CUFFT_SUCCESS) fr = cufftSetStream(p->fft, p->stream);
     if (fr != CUFFT_SUCCESS) {
       char buf[96];
       snprintf(buf, sizeof(buf), "cuFFT plan failed (%d)", (int)fr);
@@ -458,6 +484,9 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
       rc = BNFFT_E_SPECTRAL_FACTOR_VANISHES;
       goto fail;
     }
+    rc = dist_create(p);   // multi-GPU transport and slab buffers (nranks > 1)
+    if (rc != BNFFT_OK) goto fail;
+    CK(cudaStreamSynchronize(p->stream), "plan sync");
   }
 #undef CK
   *out = p;
@@ -475,6 +504,15 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
     return BNFFT_E_INVALID_ARG;
   }
   cudaSetDevice(p->device);
+  if (p->dist) return dist_set_nodes(p, n, x, first_bad);
+  return local_set_nodes(p, n, x, first_bad);
+}
+
+}  // extern "C"
+
+// the one-rank body of bnfft_set_nodes (also the owner-side step of BNFFT_DIST_SLAB)
+int bnfft::local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad) {
+  if (first_bad) *first_bad = -1;
   p->nodes_set = false;
   cudaError_t e;
   if (n > p->cap) {
@@ -490,14 +528,14 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
   int64_t ntiles = (std::max<int64_t>(n, 1) + kSortTile - 1) / kSortTile;
   int64_t nh = ((int64_t)1 << std::max(p->digit_bits, 1)) * ntiles;
   if (nh > p->hist_cap) {
-    dfree(p->d_hist);
+    dfree_plan(p, p->d_hist);
     p->d_hist = nullptr;
     if ((e = dmalloc(p, &p->d_hist, nh * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "alloc hist");
     p->hist_cap = nh;
   }
   int64_t np = (nh + 4095) / 4096 + 1;
   if (np > p->part_cap) {
-    dfree(p->d_scan_part);
+    dfree_plan(p, p->d_scan_part);
     p->d_scan_part = nullptr;
     if ((e = dmalloc(p, &p->d_scan_part, np * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "alloc scan");
     p->part_cap = np;
@@ -507,7 +545,7 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
     int64_t nblk = n > 0 ? ((n - 1) >> p->ub_log2) + 1 : 1;
     p->nkeys = nblk * p->nbins;
     if (p->nkeys + 1 > p->key_start_cap) {
-      dfree(p->d_bin_start);
+      dfree_plan(p, p->d_bin_start);
       p->d_bin_start = nullptr;
       if ((e = dmalloc(p, &p->d_bin_start, (p->nkeys + 1) * sizeof(uint32_t))) != cudaSuccess)
         return cuda_fail(e, "alloc key offsets");
@@ -527,7 +565,7 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
   if (p->opts.flags & BNFFT_PRECOMPUTE_PSI) {   // Algorithm 2 step 0(b)
     const size_t wb = (size_t)std::max<int64_t>(n, 1) * ((2 * p->opts.m + 3) / 4 * 4) * (p->csize / 2);   // rows padded to 16 B
     if (n > p->pre_cap) {
-      dfree(p->d_pre_w);
+      dfree_plan(p, p->d_pre_w);
       p->d_pre_w = nullptr;
       if ((e = dmalloc(p, &p->d_pre_w, wb)) != cudaSuccess) return cuda_fail(e, "alloc psi table");
       p->pre_cap = std::max<int64_t>(n, 1);
@@ -567,13 +605,17 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
   return BNFFT_OK;
 }
 
+extern "C" {
+
 int bnfft_execute(bnfft_plan_s* p, const void* fhat, void* f) {
   if (!p) return BNFFT_E_INVALID_ARG;
   if (!p->nodes_set) { set_error("call bnfft_set_nodes first"); return BNFFT_E_NODES_NOT_SET; }
-  if (!fhat || (p->n > 0 && !f)) { set_error("NULL buffer"); return BNFFT_E_INVALID_ARG; }
+  const int64_t n_out = (p->dist && p->opts.dist == BNFFT_DIST_SLAB) ? 1 : p->n;
+  if (!fhat || (n_out > 0 && !f)) { set_error("NULL buffer"); return BNFFT_E_INVALID_ARG; }
   cudaSetDevice(p->device);
   cudaError_t e;
   if ((e = join_precompute(p)) != cudaSuccess) return cuda_fail(e, "precompute join");
+  if (p->dist && p->opts.dist == BNFFT_DIST_SLAB) return dist_execute(p, fhat, f);
   cudaEvent_t ev;
   timer_begin(p, ST_DECONV, &ev);
   if ((e = launch_deconv(p, fhat)) != cudaSuccess) return cuda_fail(e, "deconv kernel");
@@ -638,8 +680,8 @@ int bnfft_transform_host(bnfft_plan_s* p, int64_t n, const double* x_host, const
   size_t fhb = (size_t)p->Md * p->opts.batch * p->csize;
   size_t fb = (size_t)n * p->opts.batch * p->csize;
   if (n > p->x_stage_cap) {
-    dfree(p->d_x_stage);
-    dfree(p->d_f_stage);
+    dfree_plan(p, p->d_x_stage);
+    dfree_plan(p, p->d_f_stage);
     p->d_x_stage = nullptr;
     p->d_f_stage = nullptr;
     if ((e = dmalloc(p, &p->d_x_stage, xb)) != cudaSuccess) return cuda_fail(e, "alloc x stage");
@@ -688,13 +730,14 @@ int bnfft_get_info(const bnfft_plan_s* p, bnfft_info* o) {
   o->n_nodes = p->nodes_set ? p->n : 0;
   o->grid_bytes = p->Ld * p->opts.batch * (int64_t)p->csize;
   o->device_bytes = p->device_bytes;
+  dist_fill_info(p, o);
   if (p->opts.d == 1) {
     o->gather_kernel = p->opts.batch > 1 ? BNFFT_GK_SEGMENT
                        : (p->opts.flags & BNFFT_PRECOMPUTE_PSI) ? BNFFT_GK_PRE1
                        : p->d1_binned ? BNFFT_GK_BIN1 : BNFFT_GK_WINDOW1;
   } else {
-    o->gather_kernel = (p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1) ? BNFFT_GK_COOP3
-                                                                                            : BNFFT_GK_BOX;
+    const bool coop3 = p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
+    o->gather_kernel = !coop3 ? BNFFT_GK_BOX : (p->gather_threads == 256 ? BNFFT_GK_COOP3 : BNFFT_GK_SWEEP3);
   }
   return BNFFT_OK;
 }
@@ -714,6 +757,7 @@ int bnfft_get_timing(bnfft_plan_s* p, bnfft_timing* o) {
   o->n_set_nodes = p->n_set;
   o->n_execute = p->n_exec;
   o->kernel_launches = p->launches;
+  o->ms_exchange = p->ms[ST_EXCH];
   return BNFFT_OK;
 }
 
