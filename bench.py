@@ -13,8 +13,12 @@ Workload (N=1): the largest single-GPU configuration of BASELINE.json, configs[3
 M=256, sigma=2 (L=512), m=4, N=2^26 uniform nodes, Gaussian-decay complex spectrum, sinh window,
 complex64.  --cfg selects another config.  After the headline line's own measurement, rank 0 also
 times the other configs (cfg2 complex64/complex128, cfg3, cfg5) under "variants".
-N>1 (torchrun): every rank runs the same per-GPU workload on its own node set (weak scaling,
-replicas: "replicas only").
+N>1 (torchrun): d = 3 configs (cfg4, the north_star's scaling config) split ONE problem over the ranks
+(strong scaling, "scaling": "strong"): rank r holds nodes [rN/P, (r+1)N/P) of the same node set and
+every rank the whole spectrum; the plan is BNFFT_DIST_SLAB over an NCCL communicator (slab of theta
+planes per rank, distributed slab FFT, m-halo plane exchange, node redistribution, outputs returned
+in user order: DESIGN.md §7).  d <= 2 configs run independent replicas, one node set per rank (weak
+scaling).  `--dist replicas` forces replicas for d = 3.
 
 Roofline: the dominant kernel is the gather (step 3).  Its binding resource is the FP32 (complex64)
 or FP64 (complex128) FMA pipe -- SURVEY §8(d): no config is HBM-bound -- so `roofline` reports the
@@ -63,6 +67,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-peaks", action="store_true")
+    ap.add_argument("--dist", default="auto", choices=["auto", "slab", "replicas"],
+                    help="N>1: slab = one problem split over the ranks (d = 3), replicas = one per rank")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU-oracle work per sample (all cores)")
     return ap.parse_args()
@@ -307,9 +313,9 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-def make_plan(bn, cfg, prec, window, device, stream):
+def make_plan(bn, cfg, prec, window, device, stream, dist_kw=None):
     return bn.Plan(cfg.d, cfg.M, cfg.sigma, cfg.m, window, prec, batch=cfg.batch, timing=True,
-                   device=device, stream=stream.cuda_stream)
+                   device=device, stream=stream.cuda_stream, **(dist_kw or {}))
 
 
 def time_steps(torch, plan, x_dev, fh_dev, out, steps, warmup, stream, world=1, dist=None):
@@ -335,7 +341,7 @@ def time_steps(torch, plan, x_dev, fh_dev, out, steps, warmup, stream, world=1, 
     return e0.elapsed_time(e1)
 
 
-STAGES = ("psihat", "keys", "sort", "build", "deconv", "fft", "gather")
+STAGES = ("psihat", "keys", "sort", "build", "deconv", "fft", "gather", "exchange")
 
 
 def roofline(cfg, prec, window, gather_ms, peaks, kname):
@@ -376,13 +382,16 @@ def roofline(cfg, prec, window, gather_ms, peaks, kname):
 
 
 def run_config(torch, bn, cfg, prec, window, steps, warmup, dev, local, stream, peaks,
-               world=1, rank=0, dist=None, variant=0):
+               world=1, rank=0, dist=None, variant=0, dist_kw=None):
     x_np = synth.make_nodes(cfg, variant=variant)
+    if dist_kw:   # slab split of one node set: this rank's contiguous chunk of the user order
+        lo, hi = cfg.N * rank // world, cfg.N * (rank + 1) // world
+        x_np = np.ascontiguousarray(x_np[lo:hi])
     fh_np = synth.make_spectrum(cfg, prec=prec)
     x_dev = torch.from_numpy(x_np).to(dev)
     fh_dev = torch.from_numpy(fh_np).to(dev)
-    plan = make_plan(bn, cfg, prec, window, local, stream)
-    out = torch.empty((cfg.batch, cfg.N), dtype=plan.cdtype, device=dev)
+    plan = make_plan(bn, cfg, prec, window, local, stream, dist_kw)
+    out = torch.empty((cfg.batch, x_np.shape[0]), dtype=plan.cdtype, device=dev)
     ms_total = time_steps(torch, plan, x_dev, fh_dev, out, steps, warmup, stream, world, dist)
     tm = plan.timing()
     info = plan.info()
@@ -429,28 +438,42 @@ def run_gpu(args):
     if rank == 0 and not args.no_peaks:
         peaks = bn.measure_peaks(local)
 
+    slab = world > 1 and (args.dist == "slab" or (args.dist == "auto" and cfg.d == 3))
+    dist_kw, comm = None, None
+    if slab:
+        # NCCL communicator of the library (its own ncclCommInitRank; the unique id travels over the
+        # torch process group)
+        obj = [bn.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = bn.nccl_comm_init(obj[0], world, rank, local)
+        dist_kw = dict(rank=rank, nranks=world, nccl_comm=comm, dist="slab")
+
     sampler = ClockSampler(local)
     sampler.start()        # samples from the warm-up on, through the timed region
     res = run_config(torch, bn, cfg, prec, window, args.steps, args.warmup, dev, local, stream, peaks,
-                     world, rank, dist, variant=rank)
+                     world, rank, dist, variant=0 if slab else rank, dist_kw=dist_kw)
     clocks = sampler.stop()
     if world > 1:
         dist.barrier()
     ms_total = shard.max_over_ranks(res["ms_total"], device=dev)
     ms_step = ms_total / args.steps
-    value = shard.aggregate_rate(cfg.N * cfg.batch, world, ms_step)
+    # strong scaling: all ranks together evaluate the N nodes of one problem; replicas: N per rank
+    value = cfg.N * cfg.batch / (ms_step * 1e-3) if slab else shard.aggregate_rate(cfg.N * cfg.batch, world, ms_step)
     plan, info = res["plan"], res["info"]
 
     line = None
     if rank == 0:
-        s = summary(cfg, prec, window, res, args.steps, peaks)
+        # per-rank stage rates and roofline: a slab rank evaluates its own n_owned nodes
+        s = summary(cfg.scaled(N=int(info.n_owned)) if slab else cfg, prec, window, res, args.steps, peaks)
         line = {
             "metric": METRIC,
             "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if slab else "weak",
             "vs_baseline": None, "dtype": "f64" if prec == "c128" else "f32",
             "data": "synthetic (seeded, synth/; BASELINE configs recipe)",
-            "config": dict(describe(cfg, prec, window), parallelism=f"replicas{world}"),
+            "config": dict(describe(cfg, prec, window),
+                           parallelism=(f"slab{world} (NCCL: slab FFT all-to-all, m-halo planes, node "
+                                        f"exchange)") if slab else f"replicas{world}"),
             "roofline": s["roofline"],
             "stages_ms": s["stages_ms"],
             "product_nodes_per_s": s["product_nodes_per_s"],
@@ -477,6 +500,7 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # (slab plans: transform_host runs the same collectives as set_nodes / execute)
         K = max(3, args.steps // 2)
         a.record(stream)
         for _ in range(K):
@@ -486,13 +510,19 @@ def run_gpu(args):
         torch.cuda.synchronize()
         ems = shard.max_over_ranks(a.elapsed_time(b) / K, device=dev)
         if rank == 0:
-            line["e2e"] = {"value": shard.aggregate_rate(cfg.N * cfg.batch, world, ems), "unit": "nodes/s",
+            e2e_v = cfg.N * cfg.batch / (ems * 1e-3) if slab else shard.aggregate_rate(cfg.N * cfg.batch, world, ems)
+            line["e2e"] = {"value": e2e_v, "unit": "nodes/s",
                            "ms_per_step": ems, "steps": K,
                            "h2d_bytes_per_step": int(xh.numel() * 8 + fhh.numel() * fhh.element_size()),
                            "d2h_bytes_per_step": int(fo.numel() * fo.element_size()),
                            "api": "bnfft_transform_host (pinned host buffers)"}
         del xh, fhh, fo
+    if slab and rank == 0:
+        line["slab"] = {"lo": int(info.slab_lo), "hi": int(info.slab_hi), "n_owned_rank0": int(info.n_owned),
+                        "halo_bytes": int(info.halo_bytes)}
     plan.close()
+    if comm is not None:
+        bn.nccl_comm_destroy(comm)
     x_np, fh_np = res["x_np"], res["fh_np"]
     del res
 

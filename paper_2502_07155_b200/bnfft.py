@@ -67,7 +67,7 @@ class bnfft_info(ctypes.Structure):
 
 GATHER_KERNELS = {0: "bnfft::gather1_kernel", 1: "bnfft::gather1b_kernel", 2: "bnfft::gather_kernel",
                   3: "bnfft::gatherN_kernel", 4: "bnfft::gather3c_kernel", 5: "bnfft::gather1_kernel",
-                  6: "bnfft::gather3s_kernel"}
+                  6: "bnfft::gather3s_kernel", 7: "bnfft::gather3y_kernel"}
 
 
 class bnfft_timing(ctypes.Structure):
@@ -346,6 +346,10 @@ def nccl_comm_init(uid: bytes, nranks: int, rank: int, device: int) -> int:
     buf = ctypes.create_string_buffer(uid, 128)
     check(bnfft_nccl_comm_init(buf, nranks, rank, device, ctypes.byref(h)), "bnfft_nccl_comm_init")
     return h.value
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    check(bnfft_nccl_comm_destroy(comm), "bnfft_nccl_comm_destroy")
 
 
 def torch_nccl_comm(group=None, device=None) -> int:

@@ -112,7 +112,12 @@ struct bnfft_plan_s {
   // nodes
   int64_t n = 0, cap = 0;
   bool nodes_set = false;
-  double* d_xs = nullptr;        // node copy n x d: user order (xs_user) or sorted (last radix pass)
+  double* d_xs = nullptr;        // node copy n x d: user order (xs_user) or sorted (last radix pass);
+                                 // rec3 plans: sorted 16-B node records (float4, see rec3)
+  bool rec3 = false;             // y-sweep d = 3 plans: the keys kernel writes a 16-B record per node
+                                 // (u_x, u_y, u_z as float; (c_y & 15) << 3 | (c_z & 7)) in user order
+                                 // (d_rec_user); the last radix pass gathers the records, not x
+  void* d_rec_user = nullptr;
   bool xs_user = false;          // d <= 2 user-blocked plans keep nodes in user order
   bool offsets_valid = false;    // key offsets built (lazily for xs_user plans)
   uint32_t* d_perm = nullptr;    // sorted pos -> user index
@@ -137,6 +142,8 @@ struct bnfft_plan_s {
   int gather_nslice = 1, gather_box_elems = 0, gather_bufstride = 0;
   int gather_nbuf = 2;
   int gather_threads = 256;      // threads per CTA of the d >= 2 gather launch
+  int g3_kind = 0;               // d = 3, m = 4, complex64, batch 1: 0 y-sweep (gather3y, default),
+                                 // 1 half-warp (gather3c, BNFFT_GATHER3C), 2 z-sweep (gather3s, BNFFT_GATHER3S)
   int gather_tbox[3] = {1, 1, 1};
   bool d1_binned = false;         // d = 1: bins of 2^bin_log2 cells, one radix pass, per-bin gather
   void* d_pre_w = nullptr;        // BNFFT_PRECOMPUTE_PSI: [n][2m] weights of the sorted nodes

@@ -13,14 +13,25 @@ const void* gather3s_kernel_ptr(bool poly);
 size_t gather3s_smem();
 int gather3s_threads();
 int gather3s_row_stride();
+const void* gather3y_kernel_ptr(bool poly);
+size_t gather3y_smem();
+int gather3y_threads();
+void gather3y_box(int* ext);
 
-// d = 3, m = 4, complex64, batch 1: bins of 8 x 8 x 16 cells and a specialised kernel -- the half-warp
-// kernel gather3c by default; the z-sweep kernel (gather3s.cu) with BNFFT_GATHER3S set at plan
-// creation (measured slower on cfg4: DESIGN.md §8)
+// d = 3, m = 4, complex64, batch 1: a specialised kernel chosen at plan creation (p->g3_kind) -- the
+// y-sweep kernel gather3y (gather3y.cu, x-line bins of 1 x 16 x 8 cells) by default; the half-warp
+// kernel gather3c (BNFFT_GATHER3C) and the z-sweep kernel gather3s (BNFFT_GATHER3S, gather3s.cu) on
+// bins of 8 x 8 x 16 cells (measured slower on cfg4: DESIGN.md §8)
 static bool use_coop3(const bnfft_plan_s* p) {
   return p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
 }
-static bool use_sweep3(const bnfft_plan_s* p) { return use_coop3(p) && getenv("BNFFT_GATHER3S"); }
+static bool use_sweep3(const bnfft_plan_s* p) { return use_coop3(p) && p->g3_kind == 2; }
+static bool use_ysweep3(const bnfft_plan_s* p) { return use_coop3(p) && p->g3_kind == 0; }
+static const void* coop3_kernel(const bnfft_plan_s* p) {
+  if (p->g3_kind == 0) return gather3y_kernel_ptr(p->tap_poly);
+  if (p->g3_kind == 2) return gather3s_kernel_ptr(p->tap_poly);
+  return p->tap_poly ? gather3c_kernel_p() : gather3c_kernel_e();
+}
 
 static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false, bool pre = false,
                                 bool binned = false) {
@@ -65,6 +76,7 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   for (int t = 0; t < d; ++t) ext[t] = (1 << p->bin_log2[t]) + T - 1;
   if (!p->c128) ext[d - 1] = (1 << p->bin_log2[d - 1]) + T;   // even start shift + 16-B multiple
   if (use_coop3(p)) ext[d - 1] = use_sweep3(p) ? gather3s_row_stride() : kRow3;   // conflict-free rows
+  if (use_ysweep3(p)) gather3y_box(ext);
   size_t box_elems = 1;
   for (int t = 0; t < d; ++t) box_elems *= (size_t)ext[t];
   const size_t per = box_elems * p->csize;
@@ -81,8 +93,8 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   p->gather_box_elems = (int)box_elems;
   p->gather_bufstride = (int)(buf_bytes / p->csize);
   for (int t = 0; t < 3; ++t) p->gather_tbox[t] = t < d ? ext[t] : 1;
-  p->gather_smem = use_sweep3(p) ? gather3s_smem() : nbuf * buf_bytes;
-  p->gather_threads = use_sweep3(p) ? gather3s_threads() : kGatherThreads;
+  p->gather_smem = use_sweep3(p) ? gather3s_smem() : use_ysweep3(p) ? gather3y_smem() : nbuf * buf_bytes;
+  p->gather_threads = use_sweep3(p) ? gather3s_threads() : use_ysweep3(p) ? gather3y_threads() : kGatherThreads;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0, nsm = 0, dev = 0;
@@ -145,6 +157,7 @@ constexpr int kMaxSegPerRound = 32;
 cudaError_t gather_prepare(bnfft_plan_s* p) {
   const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1,
                                  (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0, p->d1_binned);
+  if (use_coop3(p)) fn = coop3_kernel(p);
   if (!fn) return cudaErrorInvalidValue;
   if (p->d1_binned) {
     // one window per bin (bin + halo, 16-byte aligned), double-buffered; persistent grid by occupancy
@@ -232,6 +245,8 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
   gp.xs_user = p->xs_user ? 1 : 0;
   gp.pre_w = (R*)p->d_pre_w;
   gp.sorted_out = (p->opts.flags & BNFFT_SORTED_OUTPUT) ? 1 : 0;
+  gp.l2_hint = 3;   // y-sweep kernel: streaming outputs must not evict the grid boxes' halos from L2
+  if (const char* s = getenv("BNFFT_L2_HINT")) gp.l2_hint = atoi(s);   // tuning knob (A/B)
   constexpr int NC = PolyN<R>::NC;
   constexpr int NH = PolyH<R>::NH;
   static_assert(2 * NH == NC, "even/odd split of the tap polynomials");
@@ -263,6 +278,15 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
       while (((int64_t)1 << mb) < mx) ++mb;
       gp.morton_bits = mb;
       gp.nkeys_morton = (p->nkeys / p->nbins) << (3 * mb);
+      if (use_ysweep3(p)) {   // items of 8 x-lines; Morton order with per-dimension bit counts
+        int bsum = 0;
+        for (int64_t dim : {(p->L + 7) >> 3, p->nb_dim[1], p->nb_dim[2]}) {
+          int b = 0;
+          while (((int64_t)1 << b) < dim) ++b;
+          bsum += b;
+        }
+        gp.nkeys_morton = (int64_t)1 << bsum;
+      }
     }
     void* args2[] = {&gp, &p->d_tmap};
     unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p->gather_grid1, p->nkeys));
@@ -294,9 +318,7 @@ cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
   const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1,
                                  (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0, p->d1_binned);
   // d = 3, m = 4, complex64: the kernel chosen at plan creation (its launch shape is in the plan)
-  if (use_coop3(p))
-    fn = p->gather_threads == gather3s_threads() ? gather3s_kernel_ptr(p->tap_poly)
-                                                 : (p->tap_poly ? gather3c_kernel_p() : gather3c_kernel_e());
+  if (use_coop3(p)) fn = coop3_kernel(p);
   if (!fn) return cudaErrorInvalidValue;
   return p->c128 ? launch_gather_t<double>(p, out, fn) : launch_gather_t<float>(p, out, fn);
 }

@@ -1,0 +1,402 @@
+// Row a6 for d = 3, m = 4, complex64, batch 1 (BASELINE cfg4): the y-sweep gather (default).
+//
+// Step 3 of Algorithm 2, f_j = sum_l theta_l prod_t w_t(l_t), as the separable contraction
+//     f_j = sum_a wx[a] sum_b wy[b] sum_c wz[c] theta[cx-3+a, cy-3+b, cz-3+c]          (A3, taps A6)
+// One node needs 8 x 8 x 8 grid values; at cfg4 density (0.5 nodes per cell) each grid value is
+// shared by 256 nodes.  Reading all 512 values of every node from shared memory (gather3c) makes the
+// shared-memory pipe the wall (4 KiB per node).  Here grid rows live in registers and are reused by
+// every node of a 16-column x-line:
+//
+//   * the sort key of a node (row a1) is its x-line: cells (cx, [16 by, 16 by + 16), [8 bz, 8 bz + 8))
+//     (bins of 1 x 16 x 8 cells).  A CTA owns the 8 x-lines cx = 8X..8X+7 of one (by, bz) ("item");
+//     the item's grid neighbourhood (15 x 23 x 18 complex64, zero outside I_L = reading A5 zero
+//     extension) is staged by TMA; warp w contracts x-line 8X + w;
+//   * lane (a, q) = (lane & 7, lane >> 3) holds two grid rows along z (16 values each) of x-plane
+//     cx-3+a: the rows r (box y index) of the current 8-row window with r mod 8 = q (slot 0) and
+//     q + 4 (slot 1).  The warp visits its nodes in column order (a warp-level counting sort by the
+//     y column); moving the window from column y to y+1 drops row y and loads row y+8 into the same
+//     (q, slot), so one 8-lane group loads one row per column step: a node costs ~3 shared-memory
+//     wavefronts of grid data instead of 32 (gather3c);
+//   * per node: the record (24 tap weights, computed once by one lane from the tap polynomials R1)
+//     is read from shared memory (z weights broadcast), each lane forms two 8-tap z-dots from its
+//     registers (the node's z offset selects the register window: a warp-uniform switch), scales
+//     them by wx[a] wy[b], and four nodes at a time are summed over the 32 lanes by a transposed
+//     shuffle tree (3 shuffles per node).
+//
+// The per-node arithmetic is independent of the order in which nodes are visited (fixed tap order,
+// fixed lane-to-row map, the same xor tree for every node slot), so results are bitwise reproducible
+// and equal for any permutation of the node set.
+#include <cuda.h>
+
+#include "gather_impl.cuh"
+
+namespace bnfft {
+namespace g3y {
+
+constexpr int NW = 16, NT = NW * 32;       // two teams of 8 warps; warp w of a team: x-line 8X + w
+constexpr int NBUF = 3;                    // box ring: the teams' current items and the next one
+constexpr int T = 8;                       // 2m taps per dimension, m = 4
+constexpr int BX = 15, BY = 23, BZ = 18;   // box extents: 8 + 7, 16 + 7, 8 + 8 (+2: x-plane stride of
+                                           // 23*18*8 B = 112 mod 128 -> conflict-free row loads)
+constexpr int BOX = BX * BY * BZ;          // complex64 elements
+constexpr int BOXB = (BOX * 8 + 127) / 128 * 128;
+constexpr int CAP = 128;                   // nodes per warp chunk (x-lines with more nodes are chunked)
+constexpr int REC = 28;                    // words per record (112 B: 16-B slots of 8 consecutive lanes'
+                                           // records distinct): wz[8] | wy pairs[8] | wx[8] | meta dst
+constexpr int OFF_REC = NBUF * BOXB;                           // float [NW][32][REC]
+constexpr int OFF_IDX = OFF_REC + NW * 32 * REC * 4;           // uint8 [NW][CAP]: sorted pos -> chunk index
+constexpr int OFF_META = OFF_IDX + NW * CAP;                   // uint8 [NW][CAP]: col << 3 | oz (sorted)
+constexpr int SMEM = OFF_META + NW * CAP;
+static_assert(OFF_REC % 16 == 0, "16-B aligned records");
+
+}  // namespace g3y
+
+size_t gather3y_smem() { return (size_t)g3y::SMEM; }
+int gather3y_threads() { return g3y::NT; }
+void gather3y_box(int* ext) {
+  ext[0] = g3y::BX;
+  ext[1] = g3y::BY;
+  ext[2] = g3y::BZ;
+}
+
+// Items: groups of 8 x-lines (X, by, bz), visited in a Morton order with unequal bit counts per
+// dimension (dense for power-of-two grids: every virtual index is a real item).  Item k of a CTA is
+// the virtual index blockIdx.x + k * gridDim.x, so consecutive CTAs work on neighbouring items and
+// their boxes' halos are served from L2.
+struct Geo3y {
+  int bx, byb, bzb;   // bits per dimension (X, by, bz)
+  int nX, nY, nZ;     // items per dimension
+};
+
+__device__ __forceinline__ bool g3y_decode(const Geo3y& g, uint32_t v, int& X, int& Y, int& Z) {
+  X = Y = Z = 0;
+  int bit = 0;
+#pragma unroll
+  for (int l = 0; l < 10; ++l) {
+    if (l < g.bzb) { Z |= (int)((v >> bit) & 1u) << l; ++bit; }
+    if (l < g.byb) { Y |= (int)((v >> bit) & 1u) << l; ++bit; }
+    if (l < g.bx) { X |= (int)((v >> bit) & 1u) << l; ++bit; }
+  }
+  return X < g.nX && Y < g.nY && Z < g.nZ;
+}
+
+// Load item k (virtual index v) into box buffer b, or complete the buffer's phase without data for a
+// hole of the virtual index space (thread of the producing warp only).
+__device__ __forceinline__ void g3y_produce(const GatherParams<float>& p, const CUtensorMap* tm, const Geo3y& g,
+                                            uint32_t v, float2* box, uint64_t* bar, uint64_t pol) {
+  int X, Y, Z;
+  if (!g3y_decode(g, v, X, Y, Z)) {
+    mbar_arrive(bar);
+    return;
+  }
+  const int c0 = Z * 8 - 4;    // z (innermost): even start (16-B aligned rows), one extra element
+  const int c1 = Y * 16 - 3;   // y
+  const int c2 = X * 8 - 3;    // x
+  mbar_expect_tx(bar, (uint32_t)(g3y::BOX * sizeof(float2)));
+  const uint32_t d = smem_u32(box), b = smem_u32(bar);
+  const uint64_t t = reinterpret_cast<uint64_t>(tm);
+  if (p.l2_hint & 2)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(d), "l"(t), "r"(b), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(d), "l"(t), "r"(b), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+// Phase A: the chunk's nodes [cb, ce) (<= CAP) sorted by y column (warp-level counting sort, stable):
+// idx[pos] = chunk index of the node at sorted position pos, meta[pos] = its (col << 3 | oz).
+__device__ __forceinline__ void g3y_phase_a(const GatherParams<float>& p, uint32_t cb, uint32_t ce,
+                                            uint8_t* idx, uint8_t* meta, int lane) {
+  constexpr int R = g3y::CAP / 32;
+  int col[R], rk[R];
+  uint32_t md[R], cnt[R];   // cnt: lane c < 16 counts nodes of column c in round r
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t i = cb + (uint32_t)(r * 32 + lane);
+    const bool valid = i < ce;
+    col[r] = 16 + lane;   // distinct dummy keys for invalid lanes
+    md[r] = 0;
+    if (valid) {          // the sorted 16-B record of the keys kernel (rec3): cell in the x-line bin
+      md[r] = __float_as_uint(__ldg(reinterpret_cast<const float*>(p.xs) + 4 * (size_t)i + 3));
+      col[r] = (int)(md[r] >> 3);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, col[r]);
+    rk[r] = __popc(peers & ((1u << lane) - 1u));
+    const unsigned vb = __ballot_sync(0xffffffffu, valid);
+    unsigned msk = vb;
+#pragma unroll
+    for (int bit = 0; bit < 4; ++bit) {
+      const unsigned bb = __ballot_sync(0xffffffffu, (col[r] >> bit) & 1);
+      msk &= ((lane >> bit) & 1) ? bb : ~bb;
+    }
+    cnt[r] = lane < 16 ? (uint32_t)__popc(msk) : 0u;
+  }
+  uint32_t tot = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) tot += cnt[r];
+  uint32_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  uint32_t base = incl - tot;   // lane c: first sorted position of column c (+ earlier rounds)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t bcol = __shfl_sync(0xffffffffu, base, col[r] & 15);
+    if (cb + (uint32_t)(r * 32 + lane) < ce) {
+      const uint32_t pos = bcol + (uint32_t)rk[r];
+      idx[pos] = (uint8_t)(r * 32 + lane);
+      meta[pos] = (uint8_t)md[r];
+    }
+    base += cnt[r];
+  }
+  __syncwarp();
+}
+
+// Phase B: records of sorted positions [s0, s0 + 32) of the chunk (lane k: position s0 + k): the 24
+// tap weights (tap polynomials, R1), the y weights as the pairs each row-lane group needs at the
+// node's column, and (column, z offset), destination.
+template <bool POLY>
+__device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32_t cb, int s0, int cn,
+                                            const uint8_t* idx, const uint8_t* meta, float* rec, int lane) {
+  constexpr int T = g3y::T;
+  const int s = s0 + lane;
+  if (s < cn) {
+    const uint32_t i = cb + idx[s];
+    const float4 c4 = __ldg(reinterpret_cast<const float4*>(p.xs) + i);
+    const uint32_t pj = __ldg(&p.perm[i]);
+    const uint32_t md = meta[s];
+    const int col = (int)(md >> 3);
+    float* r = rec + lane * g3y::REC;
+    float w[T];
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.y, p), p, w);
+    reinterpret_cast<float4*>(r)[2] = make_float4(w[0], w[1], w[2], w[3]);
+    reinterpret_cast<float4*>(r)[3] = make_float4(w[4], w[5], w[6], w[7]);
+    // row-lane group q holds window rows b = (q - col) & 7 and b ^ 4: pairs (wy[b], wy[b ^ 4])
+    float yq[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int b = (q - col) & 7;
+      yq[2 * q] = r[8 + b];
+      yq[2 * q + 1] = r[8 + (b ^ 4)];
+    }
+    reinterpret_cast<float4*>(r)[2] = make_float4(yq[0], yq[1], yq[2], yq[3]);
+    reinterpret_cast<float4*>(r)[3] = make_float4(yq[4], yq[5], yq[6], yq[7]);
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.z, p), p, w);
+    reinterpret_cast<float4*>(r)[0] = make_float4(w[0], w[1], w[2], w[3]);
+    reinterpret_cast<float4*>(r)[1] = make_float4(w[4], w[5], w[6], w[7]);
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.x, p), p, w);
+    reinterpret_cast<float4*>(r)[4] = make_float4(w[0], w[1], w[2], w[3]);
+    reinterpret_cast<float4*>(r)[5] = make_float4(w[4], w[5], w[6], w[7]);
+    reinterpret_cast<uint2*>(r)[12] = make_uint2(md, p.sorted_out ? i : pj);
+  }
+  __syncwarp();
+}
+
+// the lane's 16 z values of box row (x-plane xa, row r) into a slot
+__device__ __forceinline__ void g3y_load_row(const float2* box, int xa, int r, float2 (&R)[16]) {
+  const float4* src = reinterpret_cast<const float4*>(box + (xa * g3y::BY + r) * g3y::BZ);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4 v = src[k];
+    R[2 * k] = make_float2(v.x, v.y);
+    R[2 * k + 1] = make_float2(v.z, v.w);
+  }
+}
+
+// z-dots of both slots for a node with z offset OZ (taps at box z index OZ + 1 + c); two partial
+// sums per slot (even / odd taps) for instruction-level parallelism, added in a fixed order
+template <int OZ>
+__device__ __forceinline__ void g3y_zdot(const float2 (&R0)[16], const float2 (&R1)[16], const float4& wa,
+                                         const float4& wb, float2& d0, float2& d1) {
+  const float wz[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+  float2 e0 = make_float2(0.f, 0.f), o0 = e0, e1 = e0, o1 = e0;
+#pragma unroll
+  for (int c = 0; c < 8; c += 2) {
+    cmac(e0, wz[c], R0[OZ + 1 + c]);
+    cmac(e1, wz[c], R1[OZ + 1 + c]);
+    cmac(o0, wz[c + 1], R0[OZ + 2 + c]);
+    cmac(o1, wz[c + 1], R1[OZ + 2 + c]);
+  }
+  d0 = __fadd2_rn(e0, o0);
+  d1 = __fadd2_rn(e1, o1);
+}
+
+__device__ __forceinline__ void g3y_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <bool POLY>
+__global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_constant__ GatherParams<float> p,
+                                                              const CUtensorMap* __restrict__ tmap) {
+  using namespace g3y;
+  extern __shared__ __align__(128) unsigned char g3y_smem[];   // TMA destinations: 128-B aligned
+  __shared__ __align__(8) uint64_t full[NBUF];
+  __shared__ int s_done[NBUF];
+  __shared__ volatile int s_tag[NBUF];   // item whose box buffer b holds or is loading
+  float2* const boxes = reinterpret_cast<float2*>(g3y_smem);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int team = wid >> 3, wt = wid & 7;
+  const int la = lane & 7, lq = lane >> 3;
+  float* const rec = reinterpret_cast<float*>(g3y_smem + OFF_REC) + wid * 32 * REC;
+  uint8_t* const idx = reinterpret_cast<uint8_t*>(g3y_smem + OFF_IDX) + wid * CAP;
+  uint8_t* const meta = reinterpret_cast<uint8_t*>(g3y_smem + OFF_META) + wid * CAP;
+  float2* __restrict__ out = (float2*)p.out;
+  const uint32_t G = gridDim.x;
+  const uint32_t nvirt = (uint32_t)p.nkeys_morton;
+  Geo3y g;
+  g.nX = (int)((p.L + 7) >> 3);
+  g.nY = (int)p.nb[1];
+  g.nZ = (int)p.nb[2];
+  g.bx = g.byb = g.bzb = 0;
+  while ((1 << g.bx) < g.nX) ++g.bx;
+  while ((1 << g.byb) < g.nY) ++g.byb;
+  while ((1 << g.bzb) < g.nZ) ++g.bzb;
+  uint64_t pol_out = 0, pol_box = 0;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_out));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_box));
+  const bool hint_out = (p.l2_hint & 1) != 0;
+
+  if (tid == 0) {
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(&full[b], 1);
+      s_done[b] = 0;
+    }
+    fence_mbar_init();
+    for (int b = 0; b < NBUF; ++b) {
+      s_tag[b] = b;
+      const uint32_t v = blockIdx.x + (uint32_t)b * G;
+      if (v < nvirt) g3y_produce(p, tmap, g, v, boxes + (size_t)b * (BOXB / 8), &full[b], pol_box);
+    }
+  }
+  __syncthreads();
+
+  for (uint32_t k = (uint32_t)team;; k += 2) {
+    const uint32_t v = blockIdx.x + k * G;
+    if (v >= nvirt) break;
+    const int b = (int)(k % NBUF);
+    int X, Y, Z;
+    const bool real = g3y_decode(g, v, X, Y, Z);
+    uint32_t nb0 = 0, ne = 0;
+    const int cx = X * 8 + wt;
+    if (real && cx < (int)p.L) {
+      const int64_t key = ((int64_t)cx * p.nb[1] + Y) * p.nb[2] + Z;
+      nb0 = __ldg(&p.key_start[key]);
+      ne = __ldg(&p.key_start[key + 1]);
+    }
+    const float2* box = boxes + (size_t)b * (BOXB / 8);
+    const int xa = wt + la;          // box x index of the lane's rows
+    bool waited = false;
+    for (uint32_t cb = nb0; cb < ne || !waited; cb += CAP) {
+      const uint32_t ce = min(ne, cb + (uint32_t)CAP);
+      const int cn = cb < ne ? (int)(ce - cb) : 0;
+      if (cn > 0) g3y_phase_a(p, cb, ce, idx, meta, lane);
+      if (!waited) {
+        while (s_tag[b] != (int)k) {
+        }
+        g3y_wait(&full[b], (k / NBUF) & 1u);
+        waited = true;
+      }
+      if (cn == 0) break;
+      // ---- sweep: nodes in column order; the row window starts at the first node's column
+      float2 R0[16], R1[16];
+      int ycur = meta[0] >> 3;
+      g3y_load_row(box, xa, ycur + ((lq - ycur) & 7), R0);
+      g3y_load_row(box, xa, ycur + ((lq + 4 - ycur) & 7), R1);
+      for (int s0 = 0; s0 < cn; s0 += 32) {
+        g3y_phase_b<POLY>(p, cb, s0, cn, idx, meta, rec, lane);
+        const int nq = min(32, cn - s0);
+        float* r = rec;
+        for (int q = 0; q < nq; ++q, r += REC) {
+          const uint32_t md = reinterpret_cast<const uint32_t*>(r)[24];
+          const int col = (int)(md >> 3);
+          while (ycur < col) {   // window [ycur, ycur + 8) -> [ycur + 1, ycur + 9): row ycur + 8
+            const int rn = ycur + 8;
+            if (lq == (rn & 3)) {
+              if ((rn >> 2) & 1) g3y_load_row(box, xa, rn, R1);
+              else g3y_load_row(box, xa, rn, R0);
+            }
+            ++ycur;
+          }
+          const float4 wa = reinterpret_cast<const float4*>(r)[0];
+          const float4 wb = reinterpret_cast<const float4*>(r)[1];
+          const float2 wy = reinterpret_cast<const float2*>(r + 8)[lq];
+          float2 d0, d1;
+          switch (md & 7u) {
+            case 0: g3y_zdot<0>(R0, R1, wa, wb, d0, d1); break;
+            case 1: g3y_zdot<1>(R0, R1, wa, wb, d0, d1); break;
+            case 2: g3y_zdot<2>(R0, R1, wa, wb, d0, d1); break;
+            case 3: g3y_zdot<3>(R0, R1, wa, wb, d0, d1); break;
+            case 4: g3y_zdot<4>(R0, R1, wa, wb, d0, d1); break;
+            case 5: g3y_zdot<5>(R0, R1, wa, wb, d0, d1); break;
+            case 6: g3y_zdot<6>(R0, R1, wa, wb, d0, d1); break;
+            default: g3y_zdot<7>(R0, R1, wa, wb, d0, d1); break;
+          }
+          // y contraction of the lane's two rows, then the sum over the 4 row lanes of x-plane a;
+          // the x-plane sums overwrite the node's (consumed) z and y weights
+          float2 t = __fmul2_rn(make_float2(wy.x, wy.x), d0);
+          cmac(t, wy.y, d1);
+          t = __fadd2_rn(t, make_float2(__shfl_xor_sync(0xffffffffu, t.x, 8), __shfl_xor_sync(0xffffffffu, t.y, 8)));
+          t = __fadd2_rn(t, make_float2(__shfl_xor_sync(0xffffffffu, t.x, 16), __shfl_xor_sync(0xffffffffu, t.y, 16)));
+          if (lq == 0) reinterpret_cast<float2*>(r)[la] = t;
+        }
+        __syncwarp();
+        // ---- x contraction and store: lane k finishes sorted position s0 + k
+        if (lane < nq) {
+          const float4* rr = reinterpret_cast<const float4*>(rec + lane * REC);
+          const float4 v0 = rr[0], v1 = rr[1], v2 = rr[2], v3 = rr[3], wx0 = rr[4], wx1 = rr[5];
+          float2 f = __fmul2_rn(make_float2(wx0.x, wx0.x), make_float2(v0.x, v0.y));
+          cmac(f, wx0.y, make_float2(v0.z, v0.w));
+          cmac(f, wx0.z, make_float2(v1.x, v1.y));
+          cmac(f, wx0.w, make_float2(v1.z, v1.w));
+          cmac(f, wx1.x, make_float2(v2.x, v2.y));
+          cmac(f, wx1.y, make_float2(v2.z, v2.w));
+          cmac(f, wx1.z, make_float2(v3.x, v3.y));
+          cmac(f, wx1.w, make_float2(v3.z, v3.w));
+          const uint32_t d = reinterpret_cast<const uint32_t*>(rec + lane * REC)[25];
+          float2* dp = out + d;
+          if (hint_out)
+            asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dp), "f"(f.x),
+                         "f"(f.y), "l"(pol_out)
+                         : "memory");
+          else
+            *dp = f;
+        }
+        __syncwarp();   // records free for the next batch
+      }
+    }
+    // ---- release box buffer b; the team's last warp loads item k + NBUF into it
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const int old = atomicAdd(&s_done[b], 1);
+      if (old == 7) {
+        s_done[b] = 0;
+        const uint32_t kn = k + NBUF;
+        const uint32_t vn = blockIdx.x + kn * G;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        s_tag[b] = (int)kn;
+        __threadfence_block();
+        if (vn < nvirt) g3y_produce(p, tmap, g, vn, boxes + (size_t)b * (BOXB / 8), &full[b], pol_box);
+      }
+    }
+  }
+}
+
+const void* gather3y_kernel_ptr(bool poly) {
+  return poly ? (const void*)gather3y_kernel<true> : (const void*)gather3y_kernel<false>;
+}
+
+}  // namespace bnfft

@@ -73,6 +73,7 @@ struct GatherParams {
   int morton_bits;        // d = 3 cooperative kernel: bits per bin coordinate of the Z-order walk
   int64_t nkeys_morton;   // user blocks x 8^morton_bits
   int sorted_out;         // BNFFT_SORTED_OUTPUT: f written at the sorted position i, not at perm[i]
+  int l2_hint;            // d = 3 y-sweep kernel: bit 0 outputs stored evict-first, bit 1 grid boxes evict-last
   WinParams wp;
   alignas(16) R ceo[PolyH<R>::NH][kMaxTaps / 2][2];   // [k][i][0] = E_i coeff k, [k][i][1] = O_i
 };

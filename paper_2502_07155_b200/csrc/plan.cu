@@ -139,6 +139,8 @@ static int collect_timing(bnfft_plan_s* p) {
 
 static void free_nodes(bnfft_plan_s* p) {
   dfree_plan(p, p->d_xs);
+  dfree_plan(p, p->d_rec_user);
+  p->d_rec_user = nullptr;
   dfree_plan(p, p->d_k0);
   dfree_plan(p, p->d_k1);
   dfree_plan(p, p->d_v0);
@@ -358,12 +360,17 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   }
   lg = std::min(lg, lgL);
   int64_t nbins = 1;
-  // d = 3, m = 4, complex64, batch 1 (warp-cooperative gather): bins of 8 x 8 x 16 cells, so the
-  // innermost box extent 16 + 2m = 24 gives conflict-free shared-memory rows.
+  // d = 3, m = 4, complex64, batch 1: the y-sweep gather (gather3y) sorts by x-line, bins of
+  // 1 x 16 x 8 cells; the half-warp / z-sweep kernels (gather3c / gather3s, selectable) use bins of
+  // 8 x 8 x 16 cells (innermost box extent 16 + 2m = 24: conflict-free shared-memory rows).
   const bool coop3 = o->d == 3 && o->m == 4 && o->prec == BNFFT_C64 && o->batch == 1 && lgL >= 4;
+  p->g3_kind = getenv("BNFFT_GATHER3S") ? 2 : getenv("BNFFT_GATHER3C") ? 1 : 0;
+  p->rec3 = coop3 && p->g3_kind == 0;
   for (int t = 0; t < 3; ++t) {
-    p->bin_log2[t] = t < o->d ? ((coop3 && t == 2) ? 4 : lg) : 0;
-    p->nb_dim[t] = t < o->d ? (L + (1 << lg) - 1) >> lg : 1;
+    int lt = lg;
+    if (coop3) lt = p->g3_kind == 0 ? (t == 0 ? 0 : t == 1 ? 4 : 3) : (t == 2 ? 4 : 3);
+    p->bin_log2[t] = t < o->d ? lt : 0;
+    p->nb_dim[t] = t < o->d ? (L + (1 << lt) - 1) >> lt : 1;
     nbins *= p->nb_dim[t];
   }
   p->nbins = nbins;
@@ -519,7 +526,8 @@ int bnfft::local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t*
     free_nodes(p);
     int64_t cap = std::max<int64_t>(n, 1);
     size_t b4 = (cap + 4) * sizeof(uint32_t);   // +4: 16-byte bulk copies of permutation ranges
-    if ((e = dmalloc(p, &p->d_xs, cap * p->opts.d * sizeof(double))) != cudaSuccess ||
+    if ((p->rec3 && (e = dmalloc(p, &p->d_rec_user, cap * 16)) != cudaSuccess) ||
+        (e = dmalloc(p, &p->d_xs, cap * std::max<size_t>(p->opts.d * sizeof(double), p->rec3 ? 16 : 0))) != cudaSuccess ||
         (e = dmalloc(p, &p->d_k0, b4)) != cudaSuccess || (e = dmalloc(p, &p->d_k1, b4)) != cudaSuccess ||
         (e = dmalloc(p, &p->d_v0, b4)) != cudaSuccess || (e = dmalloc(p, &p->d_v1, b4)) != cudaSuccess)
       return cuda_fail(e, "alloc nodes");
@@ -737,7 +745,8 @@ int bnfft_get_info(const bnfft_plan_s* p, bnfft_info* o) {
                        : p->d1_binned ? BNFFT_GK_BIN1 : BNFFT_GK_WINDOW1;
   } else {
     const bool coop3 = p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
-    o->gather_kernel = !coop3 ? BNFFT_GK_BOX : (p->gather_threads == 256 ? BNFFT_GK_COOP3 : BNFFT_GK_SWEEP3);
+    o->gather_kernel = !coop3 ? BNFFT_GK_BOX
+                       : p->g3_kind == 0 ? BNFFT_GK_YSWEEP3 : p->g3_kind == 1 ? BNFFT_GK_COOP3 : BNFFT_GK_SWEEP3;
   }
   return BNFFT_OK;
 }

@@ -76,11 +76,34 @@ __device__ __forceinline__ uint32_t node_key(const double* xv, const KeyParams& 
   return code ? 0u : key;
 }
 
+// rec3 plans (y-sweep gather, d = 3): the node's record for the gather, computed here once in user
+// order -- u_t = L x_t - floor(L x_t) rounded to float (the complex64 path's u, reading A11), and
+// the cell's position in its 1 x 16 x 8 x-line bin ((c_y & 15) << 3 | (c_z & 7)); clamped cells
+// (fl(L x) == L/2) take u = 1 as in every gather.
+__device__ __forceinline__ float4 node_rec3(const double* xv, const KeyParams& kp) {
+  float u[3];
+  int c[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const double Lx = __dmul_rn(kp.Lf, xv[t]);
+    const double fl = floor(Lx);
+    double w = Lx - fl;
+    int ci = __double2int_rz(fl) + (int)(kp.L >> 1);
+    if (ci > (int)kp.L - 1) {
+      ci = (int)kp.L - 1;
+      w = 1.0;
+    }
+    u[t] = (float)w;
+    c[t] = ci;
+  }
+  return make_float4(u[0], u[1], u[2], __uint_as_float((uint32_t)(((c[1] & 15) << 3) | (c[2] & 7))));
+}
+
 template <int D>
 __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams kp,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                             unsigned long long* __restrict__ bad, double* __restrict__ xcopy,
-                            int aligned16) {
+                            int aligned16, float4* __restrict__ rec) {
   // xcopy != nullptr: user-order node copy (d <= 2 user-blocked plans: the gather reads xcopy[perm[i]]
   // inside an L2-resident user block; or no radix pass: the identity permutation).
   // vals (identity permutation) is only written when no radix pass will run; the first pass
@@ -117,6 +140,10 @@ __global__ void keys_kernel(const double* __restrict__ x, int64_t n, KeyParams k
     const uint32_t k1 = full ? node_key<D>(xv + D, kp, c1) : 0u;
     if (c0) atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)c0);
     if (c1) atomicMin(bad, ((unsigned long long)(i + 1) << 4) | (unsigned long long)c1);
+    if (D == 3 && rec) {
+      rec[i] = node_rec3(xv, kp);
+      if (full) rec[i + 1] = node_rec3(xv + D, kp);
+    }
     if (full) {
       reinterpret_cast<uint2*>(keys)[q] = make_uint2(k0, k1);
       if (vals) reinterpret_cast<uint2*>(vals)[q] = make_uint2((uint32_t)i, (uint32_t)(i + 1));
@@ -639,7 +666,8 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
     kfn<<<grid_for((n + 1) / 2, 256), 256, 0, p->stream>>>(x, n, kp, p->d_k0,
                                                            p->sort_passes ? nullptr : p->d_v0, p->d_bad,
                                                            (p->xs_user || !p->sort_passes) ? p->d_xs : nullptr,
-                                                           ((uintptr_t)x & 15) == 0 ? 1 : 0);
+                                                           ((uintptr_t)x & 15) == 0 ? 1 : 0,
+                                                           p->rec3 ? (float4*)p->d_rec_user : nullptr);
     p->launches++;
   }
   return cudaGetLastError();
@@ -718,10 +746,12 @@ cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n) {
       cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
       if (e != cudaSuccess) return e;
       const bool last = pass == p->sort_passes - 1;
+      // last pass: the sorted copy of the per-node payload -- x (d doubles), or the rec3 record
+      // (16 B = two doubles, gathered from the keys kernel's user-order records)
       scatter_for(b)<<<(unsigned)sl.ntiles, kSortThreads, 2 * kSortTile * sizeof(uint32_t), p->stream>>>(
-          kin, vin, (last && p->sort_passes == 1) ? nullptr : kout, vout, n, shift, p->d_hist, sl, x,
-          (last && !p->xs_user) ? p->d_xs : nullptr,
-          p->opts.d);
+          kin, vin, (last && p->sort_passes == 1) ? nullptr : kout, vout, n, shift, p->d_hist, sl,
+          p->rec3 ? (const double*)p->d_rec_user : x, (last && !p->xs_user) ? p->d_xs : nullptr,
+          p->rec3 ? 2 : p->opts.d);
       p->launches++;
       std::swap(kin, kout);
       if (!vin) {

@@ -1,8 +1,9 @@
 """GPU parity for the round-2 paths, through the C ABI against the CPU oracle:
 
-* the z-sweep gather (gather3s, d = 3, m = 4, complex64): clustered node sets that overflow a bin's
-  stash (chunked bins), many nodes in one cell, grid nodes (Kronecker case), the global grid ends,
-  and the half-warp kernel it replaced (BNFFT_GATHER3C) as a second witness;
+* the d = 3, m = 4, complex64 gathers (y-sweep gather3y, the default; z-sweep gather3s): clustered
+  node sets that overflow a bin's stash or an x-line's chunk, many nodes in one cell, grid nodes
+  (Kronecker case), the global grid ends, sparse node sets, several grid sizes, and the half-warp
+  kernel gather3c (BNFFT_GATHER3C) as a further witness;
 * BNFFT_SORTED_OUTPUT: f_sorted[i] == f_user[perm[i]] bitwise;
 * repeated executes on d = 2 and d = 3 plans are bitwise equal (the FFT input's zero padding is
   written once at plan creation);
@@ -58,14 +59,19 @@ def oracle_f(x, fh, M, m, window="sinh"):
     return O.algorithm2(x, fh.astype(np.complex128), M, 2.0, m, window)["f"]
 
 
-# ----------------------------------------------------------------------------- z-sweep gather
+# ----------------------------------------------------------------------------- d = 3, m = 4 gathers
+# Three kernels serve d = 3, m = 4, complex64, batch 1 (chosen at plan creation): the y-sweep kernel
+# gather3y (default: x-line bins of 1 x 16 x 8 cells, rows in registers), the half-warp kernel gather3c
+# (BNFFT_GATHER3C) and the z-sweep kernel gather3s (BNFFT_GATHER3S), both on 8 x 8 x 16-cell bins.
 def _sweep_inputs(kind, M, N, seed):
     rng = np.random.default_rng(seed)
     L = 2 * M
     if kind == "uniform":
         x = rng.random((N, 3)) - 0.5
-    elif kind == "one_bin":            # every node in one 8x8x16-cell bin: stash chunking (> 768)
+    elif kind == "one_bin":            # every node in one 8x8x16-cell bin: chunked bins / x-lines
         x = (rng.random((N, 3)) * np.array([8, 8, 16]) + np.array([3, -20, 5])) / L
+    elif kind == "one_xline":          # every node in one 1x16x8-cell x-line: > CAP nodes, chunks
+        x = (rng.random((N, 3)) * np.array([1, 16, 8]) + np.array([5, -16, 8])) / L
     elif kind == "one_cell":           # all nodes in one cell: one column, one z step
         x = (rng.random((N, 3)) + np.array([-7, 2, 11])) / L
     elif kind == "grid_nodes":         # Kronecker case u == 0 in every dimension
@@ -74,26 +80,36 @@ def _sweep_inputs(kind, M, N, seed):
         x = rng.random((N, 3)) - 0.5
         x[: N // 2, 0] = -0.5 + rng.random(N // 2) * 3 / L
         x[N // 2:, 2] = 0.5 - rng.random(N - N // 2) * 3 / L
+    elif kind == "sparse":             # a few nodes: most items and x-lines empty
+        x = rng.random((N, 3)) - 0.5
     else:
         raise ValueError(kind)
     return np.clip(x, -0.5, np.nextafter(0.5, 0))
 
 
-@pytest.fixture
-def sweep3(monkeypatch):
-    """Plans created inside the test use the z-sweep kernel (BNFFT_GATHER3S, read at plan creation)."""
-    monkeypatch.setenv("BNFFT_GATHER3S", "1")
+KERNEL3 = {"y": ("gather3y_kernel", None), "c": ("gather3c_kernel", "BNFFT_GATHER3C"),
+           "s": ("gather3s_kernel", "BNFFT_GATHER3S")}
 
 
-@pytest.mark.parametrize("kind", ["uniform", "one_bin", "one_cell", "grid_nodes", "edges"])
-def test_sweep3_parity(bn, torch, kind, sweep3):
+def _use_kernel3(monkeypatch, which):
+    monkeypatch.delenv("BNFFT_GATHER3C", raising=False)
+    monkeypatch.delenv("BNFFT_GATHER3S", raising=False)
+    env = KERNEL3[which][1]
+    if env:
+        monkeypatch.setenv(env, "1")
+
+
+@pytest.mark.parametrize("which", ["y", "s"])
+@pytest.mark.parametrize("kind", ["uniform", "one_bin", "one_xline", "one_cell", "grid_nodes", "edges", "sparse"])
+def test_sweep3_parity(bn, torch, kind, which, monkeypatch):
     M, m = 32, 4
-    N = 3000 if kind != "uniform" else 40_003
+    N = {"uniform": 40_003, "one_xline": 700, "sparse": 17}.get(kind, 3000)
     x = _sweep_inputs(kind, M, N, 11)
     cfg = synth.CONFIGS[4].scaled(M=M, N=N)
     fh = synth.make_spectrum(cfg, variant=3, prec="c64")
+    _use_kernel3(monkeypatch, which)
     f, plan = gpu_run(bn, torch, x, fh, M, m, "c64")
-    assert bn.GATHER_KERNELS[plan.info().gather_kernel].endswith("gather3s_kernel")
+    assert bn.GATHER_KERNELS[plan.info().gather_kernel].endswith(KERNEL3[which][0])
     ref = oracle_f(x, fh, M, m)
     assert rel_l2(f, ref) <= TOL["c64"]
     if kind == "grid_nodes":   # interpolation property (P:328-333): f_j == theta at the node's cell
@@ -104,29 +120,46 @@ def test_sweep3_parity(bn, torch, kind, sweep3):
     plan.close()
 
 
-def test_sweep3_vs_halfwarp_kernel(bn, torch, monkeypatch):
-    """The default half-warp kernel (gather3c) and the z-sweep kernel on the same inputs."""
+@pytest.mark.parametrize("M", [8, 24, 32])
+def test_ysweep3_grid_sizes(bn, torch, M, monkeypatch):
+    """L = 16 (one item), L = 48 (partial y bins and a partial 8-x-line item), L = 64."""
+    m, N = 4, 5000
+    x = _sweep_inputs("uniform", M, N, 13)
+    cfg = synth.CONFIGS[4].scaled(M=M, N=N)
+    fh = synth.make_spectrum(cfg, variant=5, prec="c64")
+    _use_kernel3(monkeypatch, "y")
+    f, plan = gpu_run(bn, torch, x, fh, M, m, "c64")
+    assert bn.GATHER_KERNELS[plan.info().gather_kernel].endswith("gather3y_kernel")
+    assert rel_l2(f, oracle_f(x, fh, M, m)) <= TOL["c64"]
+    plan.close()
+
+
+def test_sweep3_kernels_agree(bn, torch, monkeypatch):
+    """The three d = 3, m = 4 kernels on the same inputs: each within tolerance of the oracle and
+    within 1e-6 of each other."""
     M, m, N = 32, 4, 20_001
     cfg = synth.CONFIGS[4].scaled(M=M, N=N)
     x = synth.make_nodes(cfg, variant=2)
     fh = synth.make_spectrum(cfg, variant=2, prec="c64")
-    f2, p2 = gpu_run(bn, torch, x, fh, M, m, "c64")
-    assert bn.GATHER_KERNELS[p2.info().gather_kernel].endswith("gather3c_kernel")
-    monkeypatch.setenv("BNFFT_GATHER3S", "1")
-    f1, p1 = gpu_run(bn, torch, x, fh, M, m, "c64")
-    assert bn.GATHER_KERNELS[p1.info().gather_kernel].endswith("gather3s_kernel")
     ref = oracle_f(x, fh, M, m)
-    assert rel_l2(f1, ref) <= TOL["c64"] and rel_l2(f2, ref) <= TOL["c64"]
-    assert rel_l2(f1, f2) <= 1e-6
-    p1.close()
-    p2.close()
+    res = {}
+    for which in ("y", "c", "s"):
+        _use_kernel3(monkeypatch, which)
+        f, p = gpu_run(bn, torch, x, fh, M, m, "c64")
+        assert bn.GATHER_KERNELS[p.info().gather_kernel].endswith(KERNEL3[which][0])
+        assert rel_l2(f, ref) <= TOL["c64"], which
+        res[which] = f
+        p.close()
+    assert rel_l2(res["y"], res["c"]) <= 1e-6 and rel_l2(res["s"], res["c"]) <= 1e-6
 
 
-def test_sweep3_repeat_bitwise(bn, torch, sweep3):
+@pytest.mark.parametrize("which", ["y", "s"])
+def test_sweep3_repeat_bitwise(bn, torch, which, monkeypatch):
     M, m, N = 32, 4, 30_000
     cfg = synth.CONFIGS[4].scaled(M=M, N=N)
     x = synth.make_nodes(cfg, variant=4)
     fh = synth.make_spectrum(cfg, variant=4, prec="c64")
+    _use_kernel3(monkeypatch, which)
     f1, plan = gpu_run(bn, torch, x, fh, M, m, "c64")
     ft = torch.from_numpy(fh).to("cuda:0")
     for _ in range(3):
@@ -136,8 +169,6 @@ def test_sweep3_repeat_bitwise(bn, torch, sweep3):
     plan.set_nodes(torch.from_numpy(np.ascontiguousarray(x[perm])).to("cuda:0"))
     assert np.array_equal(plan.execute(ft).cpu().numpy()[0], f1[0][perm])
     plan.close()
-
-
 # ----------------------------------------------------------------------------- sorted output
 @pytest.mark.parametrize("d,M,m,prec", [(1, 1 << 12, 8, "c64"), (1, 1 << 16, 8, "c128"), (2, 64, 6, "c64"),
                                         (3, 32, 4, "c64"), (3, 16, 3, "c128")])
@@ -245,7 +276,8 @@ def test_slab_ranks(bn, torch, P, prec, balanced, kind):
     # must equal what the ranks agreed on from their device histograms (all-gathered)
     c = np.minimum(np.floor(L * x[:, 1]).astype(np.int64) + L // 2, L - 1)
     hist = np.bincount(c, minlength=L)
-    exp = bn.slab_cuts(L, P, 8, hist if balanced else None)
+    align = 1 << info[0].bin_log2[1]      # cut points are whole bins of the sort (row a1)
+    exp = bn.slab_cuts(L, P, align, hist if balanced else None)
     assert lo + [hi[-1]] == list(exp)
     assert [i.n_owned for i in info] == [int(hist[exp[r]:exp[r + 1]].sum()) for r in range(P)]
 
