@@ -134,8 +134,10 @@ typedef struct {
 /* Plan description.  Node binning geometry (for the stable bin sort, row a1): the cell of
  * a node is c_t = floor(L x_t) + L/2 in [0, L) (clamped to L-1), its bin b_t = c_t >> bin_log2[t],
  * its bin index is row-major (dim 0 slowest) over bins_per_dim, and its sort key is
- * (j >> user_block_log2) * nbins + bin for user index j.  Nodes are sorted stably by that key
- * (ties by user index); nkeys = ceil(n / 2^user_block_log2) * nbins for the current node set.
+ * ((j >> user_block_log2) * nbins + bin) * 2^key_col_bits + (c_1 mod 2^key_col_bits) for user index
+ * j (key_col_bits = 4 for the d = 3 y-sweep gather: an x-line bin's nodes in y-column order, else 0).
+ * Nodes are sorted stably by that key (ties by user index); the key offsets (bnfft_get_bin_offsets)
+ * are per (user block, bin): nkeys = ceil(n / 2^user_block_log2) * nbins for the current node set.
  * tap_poly: the gather evaluates psi by per-tap polynomials (fit error tap_fit_err, checked at
  * plan creation) rather than by direct sinc * phi evaluation. */
 typedef struct {
@@ -165,6 +167,7 @@ typedef struct {
   int64_t slab_lo, slab_hi; /* DIST_SLAB: this rank's planes [slab_lo, slab_hi) of dimension 2 */
   int64_t n_owned;          /* DIST_SLAB: nodes this rank evaluates (its slab's nodes)      */
   int64_t halo_bytes;       /* DIST_SLAB: grid bytes received from the neighbours per execute */
+  int32_t key_col_bits;     /* minor sort digit below the bin (see above)                  */
 } bnfft_info;
 
 /* bnfft_info.gather_kernel */

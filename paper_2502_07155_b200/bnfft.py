@@ -62,7 +62,7 @@ class bnfft_info(ctypes.Structure):
                 ("tap_fit_err", c_double), ("key_bits", c_int32), ("sort_passes", c_int32), ("flatness", c_double),
                 ("n_nodes", c_int64), ("grid_bytes", c_int64), ("device_bytes", c_int64),
                 ("gather_kernel", c_int32), ("rank", c_int32), ("nranks", c_int32), ("dist", c_int32),
-                ("slab_lo", c_int64), ("slab_hi", c_int64), ("n_owned", c_int64), ("halo_bytes", c_int64)]
+                ("slab_lo", c_int64), ("slab_hi", c_int64), ("n_owned", c_int64), ("halo_bytes", c_int64), ("key_col_bits", c_int32)]
 
 
 GATHER_KERNELS = {0: "bnfft::gather1_kernel", 1: "bnfft::gather1b_kernel", 2: "bnfft::gather_kernel",

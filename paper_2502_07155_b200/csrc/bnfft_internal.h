@@ -88,6 +88,8 @@ struct bnfft_plan_s {
   int64_t nb_dim[3] = {1, 1, 1};
   int64_t nbins = 1;
   int key_bits = 0, sort_passes = 0, digit_bits = 0;
+  int col_bits = 0;            // rec3: minor sort digit c_1 mod 16 below the bin (nodes of an x-line in
+                               // column order); key offsets stay per bin
   int ub_log2 = 31;            // user-block size of the sort key (user block, bin); 31 = one block
   int64_t nkeys = 1;           // number of (user block, bin) keys of the current node set
   int64_t key_start_cap = 0;

@@ -7,25 +7,31 @@
 // shared-memory pipe the wall (4 KiB per node).  Here grid rows live in registers and are reused by
 // every node of a 16-column x-line:
 //
-//   * the sort key of a node (row a1) is its x-line: cells (cx, [16 by, 16 by + 16), [8 bz, 8 bz + 8))
-//     (bins of 1 x 16 x 8 cells).  A CTA owns the 8 x-lines cx = 8X..8X+7 of one (by, bz) ("item");
-//     the item's grid neighbourhood (15 x 23 x 18 complex64, zero outside I_L = reading A5 zero
-//     extension) is staged by TMA; warp w contracts x-line 8X + w;
+//   * sort (row a1): the key of a node is its x-line bin (cells cx x [16 by, 16 by + 16) x
+//     [8 bz, 8 bz + 8), bins of 1 x 16 x 8 cells) with the y column c_y mod 16 as a minor digit, so
+//     an x-line's nodes arrive in column order; the keys kernel writes a 16-B record per node
+//     (u_x, u_y, u_z as float, column and z offset) that the last radix pass gathers (rec3);
+//   * a CTA of 16 warps = two teams of 8; an item = the 8 x-lines cx = 8X..8X+7 of one (by, bz),
+//     warp w of a team contracts x-line 8X + w; items alternate between the teams and their grid
+//     neighbourhoods (15 x 23 x 18 complex64, zero outside I_L = reading A5 zero extension) are
+//     staged by TMA in a ring of three box buffers, so the next item's box is in flight while both
+//     teams compute (mbarrier per buffer; the last warp of a team to release a box loads the item
+//     three ahead into it);
 //   * lane (a, q) = (lane & 7, lane >> 3) holds two grid rows along z (16 values each) of x-plane
 //     cx-3+a: the rows r (box y index) of the current 8-row window with r mod 8 = q (slot 0) and
-//     q + 4 (slot 1).  The warp visits its nodes in column order (a warp-level counting sort by the
-//     y column); moving the window from column y to y+1 drops row y and loads row y+8 into the same
-//     (q, slot), so one 8-lane group loads one row per column step: a node costs ~3 shared-memory
-//     wavefronts of grid data instead of 32 (gather3c);
-//   * per node: the record (24 tap weights, computed once by one lane from the tap polynomials R1)
-//     is read from shared memory (z weights broadcast), each lane forms two 8-tap z-dots from its
-//     registers (the node's z offset selects the register window: a warp-uniform switch), scales
-//     them by wx[a] wy[b], and four nodes at a time are summed over the 32 lanes by a transposed
-//     shuffle tree (3 shuffles per node).
+//     q + 4 (slot 1).  Moving the window from column y to y+1 drops row y and loads row y+8 into the
+//     same (q, slot), so one 8-lane group loads one row per column step: grid data costs ~3 shared-
+//     memory wavefronts per node instead of 32 (gather3c);
+//   * per batch of 32 nodes each lane evaluates one node's 24 tap weights (tap polynomials, R1) into
+//     a shared-memory record; per node the warp reads the record (z weights broadcast, y weights
+//     pre-rotated to the lane groups), each lane forms two 8-tap z-dots from its registers (the
+//     node's z offset selects the register window: a warp-uniform switch), contracts its two rows
+//     with wy, the 4 row lanes of each x-plane are summed by two shuffles, and after the batch each
+//     lane finishes one node's x contraction (sum_a wx[a] P_a) and stores it.
 //
 // The per-node arithmetic is independent of the order in which nodes are visited (fixed tap order,
-// fixed lane-to-row map, the same xor tree for every node slot), so results are bitwise reproducible
-// and equal for any permutation of the node set.
+// fixed lane-to-row map, fixed shuffle tree), so results are bitwise reproducible and equal for any
+// permutation of the node set.
 #include <cuda.h>
 
 #include "gather_impl.cuh"
@@ -40,13 +46,10 @@ constexpr int BX = 15, BY = 23, BZ = 18;   // box extents: 8 + 7, 16 + 7, 8 + 8 
                                            // 23*18*8 B = 112 mod 128 -> conflict-free row loads)
 constexpr int BOX = BX * BY * BZ;          // complex64 elements
 constexpr int BOXB = (BOX * 8 + 127) / 128 * 128;
-constexpr int CAP = 128;                   // nodes per warp chunk (x-lines with more nodes are chunked)
 constexpr int REC = 28;                    // words per record (112 B: 16-B slots of 8 consecutive lanes'
                                            // records distinct): wz[8] | wy pairs[8] | wx[8] | meta dst
 constexpr int OFF_REC = NBUF * BOXB;                           // float [NW][32][REC]
-constexpr int OFF_IDX = OFF_REC + NW * 32 * REC * 4;           // uint8 [NW][CAP]: sorted pos -> chunk index
-constexpr int OFF_META = OFF_IDX + NW * CAP;                   // uint8 [NW][CAP]: col << 3 | oz (sorted)
-constexpr int SMEM = OFF_META + NW * CAP;
+constexpr int SMEM = OFF_REC + NW * 32 * REC * 4;
 static_assert(OFF_REC % 16 == 0, "16-B aligned records");
 
 }  // namespace g3y
@@ -106,70 +109,19 @@ __device__ __forceinline__ void g3y_produce(const GatherParams<float>& p, const 
         ::"r"(d), "l"(t), "r"(b), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 
-// Phase A: the chunk's nodes [cb, ce) (<= CAP) sorted by y column (warp-level counting sort, stable):
-// idx[pos] = chunk index of the node at sorted position pos, meta[pos] = its (col << 3 | oz).
-__device__ __forceinline__ void g3y_phase_a(const GatherParams<float>& p, uint32_t cb, uint32_t ce,
-                                            uint8_t* idx, uint8_t* meta, int lane) {
-  constexpr int R = g3y::CAP / 32;
-  int col[R], rk[R];
-  uint32_t md[R], cnt[R];   // cnt: lane c < 16 counts nodes of column c in round r
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t i = cb + (uint32_t)(r * 32 + lane);
-    const bool valid = i < ce;
-    col[r] = 16 + lane;   // distinct dummy keys for invalid lanes
-    md[r] = 0;
-    if (valid) {          // the sorted 16-B record of the keys kernel (rec3): cell in the x-line bin
-      md[r] = __float_as_uint(__ldg(reinterpret_cast<const float*>(p.xs) + 4 * (size_t)i + 3));
-      col[r] = (int)(md[r] >> 3);
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, col[r]);
-    rk[r] = __popc(peers & ((1u << lane) - 1u));
-    const unsigned vb = __ballot_sync(0xffffffffu, valid);
-    unsigned msk = vb;
-#pragma unroll
-    for (int bit = 0; bit < 4; ++bit) {
-      const unsigned bb = __ballot_sync(0xffffffffu, (col[r] >> bit) & 1);
-      msk &= ((lane >> bit) & 1) ? bb : ~bb;
-    }
-    cnt[r] = lane < 16 ? (uint32_t)__popc(msk) : 0u;
-  }
-  uint32_t tot = 0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) tot += cnt[r];
-  uint32_t incl = tot;
-#pragma unroll
-  for (int o = 1; o < 16; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  uint32_t base = incl - tot;   // lane c: first sorted position of column c (+ earlier rounds)
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t bcol = __shfl_sync(0xffffffffu, base, col[r] & 15);
-    if (cb + (uint32_t)(r * 32 + lane) < ce) {
-      const uint32_t pos = bcol + (uint32_t)rk[r];
-      idx[pos] = (uint8_t)(r * 32 + lane);
-      meta[pos] = (uint8_t)md[r];
-    }
-    base += cnt[r];
-  }
-  __syncwarp();
-}
-
-// Phase B: records of sorted positions [s0, s0 + 32) of the chunk (lane k: position s0 + k): the 24
-// tap weights (tap polynomials, R1), the y weights as the pairs each row-lane group needs at the
-// node's column, and (column, z offset), destination.
+// Phase B: records of sorted nodes [s0, min(s0 + 32, e)) (lane k: node s0 + k; the sort key's minor
+// digit puts an x-line's nodes in y-column order): the 24 tap weights (tap polynomials, R1), the y
+// weights as the pairs each row-lane group needs at the node's column, (column, z offset) and the
+// destination.  Reads the keys kernel's sorted 16-B records (rec3), coalesced.
 template <bool POLY>
-__device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32_t cb, int s0, int cn,
-                                            const uint8_t* idx, const uint8_t* meta, float* rec, int lane) {
+__device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32_t s0, uint32_t e, float* rec,
+                                            int lane) {
   constexpr int T = g3y::T;
-  const int s = s0 + lane;
-  if (s < cn) {
-    const uint32_t i = cb + idx[s];
+  const uint32_t i = s0 + (uint32_t)lane;
+  if (i < e) {
     const float4 c4 = __ldg(reinterpret_cast<const float4*>(p.xs) + i);
     const uint32_t pj = __ldg(&p.perm[i]);
-    const uint32_t md = meta[s];
+    const uint32_t md = __float_as_uint(c4.w);
     const int col = (int)(md >> 3);
     float* r = rec + lane * g3y::REC;
     float w[T];
@@ -251,8 +203,6 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
   const int team = wid >> 3, wt = wid & 7;
   const int la = lane & 7, lq = lane >> 3;
   float* const rec = reinterpret_cast<float*>(g3y_smem + OFF_REC) + wid * 32 * REC;
-  uint8_t* const idx = reinterpret_cast<uint8_t*>(g3y_smem + OFF_IDX) + wid * CAP;
-  uint8_t* const meta = reinterpret_cast<uint8_t*>(g3y_smem + OFF_META) + wid * CAP;
   float2* __restrict__ out = (float2*)p.out;
   const uint32_t G = gridDim.x;
   const uint32_t nvirt = (uint32_t)p.nkeys_morton;
@@ -298,26 +248,18 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
     }
     const float2* box = boxes + (size_t)b * (BOXB / 8);
     const int xa = wt + la;          // box x index of the lane's rows
-    bool waited = false;
-    for (uint32_t cb = nb0; cb < ne || !waited; cb += CAP) {
-      const uint32_t ce = min(ne, cb + (uint32_t)CAP);
-      const int cn = cb < ne ? (int)(ce - cb) : 0;
-      if (cn > 0) g3y_phase_a(p, cb, ce, idx, meta, lane);
-      if (!waited) {
-        while (s_tag[b] != (int)k) {
-        }
-        g3y_wait(&full[b], (k / NBUF) & 1u);
-        waited = true;
-      }
-      if (cn == 0) break;
+    if (nb0 < ne) g3y_phase_b<POLY>(p, nb0, ne, rec, lane);   // overlaps the box's TMA
+    while (s_tag[b] != (int)k) {
+    }
+    g3y_wait(&full[b], (k / NBUF) & 1u);
+    if (nb0 < ne) {
       // ---- sweep: nodes in column order; the row window starts at the first node's column
       float2 R0[16], R1[16];
-      int ycur = meta[0] >> 3;
+      int ycur = (int)(reinterpret_cast<const uint32_t*>(rec)[24] >> 3);
       g3y_load_row(box, xa, ycur + ((lq - ycur) & 7), R0);
       g3y_load_row(box, xa, ycur + ((lq + 4 - ycur) & 7), R1);
-      for (int s0 = 0; s0 < cn; s0 += 32) {
-        g3y_phase_b<POLY>(p, cb, s0, cn, idx, meta, rec, lane);
-        const int nq = min(32, cn - s0);
+      for (uint32_t s0 = nb0;;) {
+        const int nq = (int)min(32u, ne - s0);
         float* r = rec;
         for (int q = 0; q < nq; ++q, r += REC) {
           const uint32_t md = reinterpret_cast<const uint32_t*>(r)[24];
@@ -353,7 +295,7 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
           if (lq == 0) reinterpret_cast<float2*>(r)[la] = t;
         }
         __syncwarp();
-        // ---- x contraction and store: lane k finishes sorted position s0 + k
+        // ---- x contraction and store: lane k finishes node s0 + k
         if (lane < nq) {
           const float4* rr = reinterpret_cast<const float4*>(rec + lane * REC);
           const float4 v0 = rr[0], v1 = rr[1], v2 = rr[2], v3 = rr[3], wx0 = rr[4], wx1 = rr[5];
@@ -375,6 +317,9 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
             *dp = f;
         }
         __syncwarp();   // records free for the next batch
+        s0 += 32;
+        if (s0 >= ne) break;
+        g3y_phase_b<POLY>(p, s0, ne, rec, lane);
       }
     }
     // ---- release box buffer b; the team's last warp loads item k + NBUF into it

@@ -374,7 +374,8 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     nbins *= p->nb_dim[t];
   }
   p->nbins = nbins;
-  p->key_bits = ceil_log2(nbins);
+  p->col_bits = p->rec3 ? 4 : 0;
+  p->key_bits = ceil_log2(nbins) + p->col_bits;
   p->sort_passes = (p->key_bits + kMaxDigitBits - 1) / kMaxDigitBits;
   p->digit_bits = p->sort_passes ? (p->key_bits + p->sort_passes - 1) / p->sort_passes : 0;
   // Sort key (user block, bin), row a1: for d <= 2 (grid resident in L2) nodes are binned inside
@@ -730,6 +731,7 @@ int bnfft_get_info(const bnfft_plan_s* p, bnfft_info* o) {
   o->nbins = p->nbins;
   o->user_block_log2 = p->ub_log2;
   o->nkeys = p->nkeys;
+  o->key_col_bits = p->col_bits;
   o->tap_poly = p->tap_poly ? 1 : 0;
   o->tap_fit_err = p->tap_fit_err;
   o->key_bits = p->key_bits;

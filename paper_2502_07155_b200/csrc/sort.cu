@@ -20,6 +20,7 @@ struct KeyParams {
   int64_t nb[3];
   int strict;
   double box_lo, box_hi;
+  int colbits;       // rec3 plans: minor key digit = c_1 mod 2^colbits (the y column inside the bin)
 };
 
 enum { BAD_NOT_FINITE = 1, BAD_RANGE = 2, BAD_BOX = 3 };
@@ -43,6 +44,7 @@ template <int D>
 __device__ __forceinline__ bool node_key_fast(const double* xv, const KeyParams& kp, uint32_t& key) {
   bool ok = true;
   key = 0;
+  uint32_t cy = 0;
 #pragma unroll
   for (int t = 0; t < D; ++t) {
     const double v = xv[t];
@@ -52,14 +54,16 @@ __device__ __forceinline__ bool node_key_fast(const double* xv, const KeyParams&
     int c = __double2int_rz(floor(Lx)) + (int)(kp.L >> 1);
     c = min(c, (int)kp.L - 1);
     key = key * (uint32_t)kp.nb[t] + ((uint32_t)c >> kp.log2W[t]);
+    if (t == 1) cy = (uint32_t)c;
   }
+  if (D >= 2 && kp.colbits) key = (key << kp.colbits) | (cy & ((1u << kp.colbits) - 1u));
   if (!ok) key = 0;
   return ok;
 }
 
 template <int D>
 __device__ __forceinline__ uint32_t node_key(const double* xv, const KeyParams& kp, int& code) {
-  uint32_t key = 0;
+  uint32_t key = 0, cy = 0;
   bool nonfinite = false, range = false, box = false;
 #pragma unroll
   for (int t = 0; t < D; ++t) {
@@ -71,7 +75,9 @@ __device__ __forceinline__ uint32_t node_key(const double* xv, const KeyParams& 
     int c = __double2int_rz(floor(Lx)) + (int)(kp.L >> 1);
     c = min(c, (int)kp.L - 1);         // fl(L x) == L/2 for x < 1/2 (defensive)
     key = key * (uint32_t)kp.nb[t] + ((uint32_t)c >> kp.log2W[t]);
+    if (t == 1) cy = (uint32_t)c;
   }
+  if (D >= 2 && kp.colbits) key = (key << kp.colbits) | (cy & ((1u << kp.colbits) - 1u));
   code = nonfinite ? BAD_NOT_FINITE : range ? BAD_RANGE : box ? BAD_BOX : 0;
   return code ? 0u : key;
 }
@@ -494,8 +500,12 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     if (kout) kout[pos] = kk;   // null: sorted keys not needed (one-pass sort, offsets from the histogram)
     const uint32_t vv = sval[li];
     vout[pos] = vv;
-    if (xsout)
-      for (int t = 0; t < d; ++t) xsout[(int64_t)pos * d + t] = __ldg(&xin[(int64_t)vv * d + t]);
+    if (xsout) {
+      if (d == 2)   // 16-B records (rec3): one vector load per node
+        reinterpret_cast<double2*>(xsout)[pos] = __ldg(reinterpret_cast<const double2*>(xin) + vv);
+      else
+        for (int t = 0; t < d; ++t) xsout[(int64_t)pos * d + t] = __ldg(&xin[(int64_t)vv * d + t]);
+    }
   }
 }
 
@@ -504,7 +514,8 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
 __global__ void build_kernel(const double* __restrict__ x, const uint32_t* __restrict__ perm,
                              const uint32_t* __restrict__ skeys, double* __restrict__ xs,
                              uint32_t* __restrict__ key_start, int64_t n, int d, int64_t nbins,
-                             int ub_log2, int64_t nkeys) {
+                             int ub_log2, int64_t nkeys, int colbits) {
+  // colbits: the sorted keys carry a minor digit below the bin (rec3); offsets are per bin
   // xs == nullptr: offsets only (plans that keep the nodes in user order)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -512,8 +523,8 @@ __global__ void build_kernel(const double* __restrict__ x, const uint32_t* __res
       uint32_t j = perm[i];
       for (int t = 0; t < d; ++t) xs[i * d + t] = x[(int64_t)j * d + t];
     }
-    int64_t kprev = (i == 0) ? -1 : (((i - 1) >> ub_log2) * nbins + (int64_t)skeys[i - 1]);
-    int64_t kcur = (i == n) ? nkeys : ((i >> ub_log2) * nbins + (int64_t)skeys[i]);
+    int64_t kprev = (i == 0) ? -1 : (((i - 1) >> ub_log2) * nbins + (int64_t)(skeys[i - 1] >> colbits));
+    int64_t kcur = (i == n) ? nkeys : ((i >> ub_log2) * nbins + (int64_t)(skeys[i] >> colbits));
     for (int64_t b = kprev + 1; b <= kcur; ++b) key_start[b] = (uint32_t)i;
   }
 }
@@ -642,6 +653,7 @@ static KeyParams key_params(const bnfft_plan_s* p) {
   kp.strict = (p->opts.flags & BNFFT_STRICT_DOMAIN) ? 1 : 0;
   kp.box_lo = -0.5 + (double)p->opts.m / (double)p->L;
   kp.box_hi = 0.5 - (double)p->opts.m / (double)p->L;
+  kp.colbits = p->col_bits;
   return kp;
 }
 
@@ -775,7 +787,8 @@ cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n) {
 // tile for digit `bin` (digit-major layout inside a block, hist_index).
 __global__ void offsets_from_hist_kernel(const uint32_t* __restrict__ hist_scan, SegLayout sl, int ndig,
                                          int64_t nbins, int64_t nkeys, int64_t n,
-                                         uint32_t* __restrict__ key_start) {
+                                         uint32_t* __restrict__ key_start, int colbits) {
+  // colbits: the digit is (bin, minor digit); a bin starts at its minor digit 0
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= nkeys;
        k += (int64_t)gridDim.x * blockDim.x) {
     if (k == nkeys) {
@@ -783,7 +796,7 @@ __global__ void offsets_from_hist_kernel(const uint32_t* __restrict__ hist_scan,
     } else {
       const int64_t blk = k / nbins;
       const int dg = (int)(k - blk * nbins);
-      key_start[k] = hist_scan[hist_index(sl, blk * sl.tpb, dg, ndig)];
+      key_start[k] = hist_scan[hist_index(sl, blk * sl.tpb, dg << colbits, ndig)];
     }
   }
 }
@@ -794,14 +807,14 @@ cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n) {
     sl.ntiles = (n + kSortTile - 1) / kSortTile;
     sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - kSortTileLog2));
     offsets_from_hist_kernel<<<grid_for(p->nkeys + 1, 256), 256, 0, p->stream>>>(
-        p->d_hist, sl, 1 << p->digit_bits, p->nbins, p->nkeys, n, p->d_bin_start);
+        p->d_hist, sl, 1 << p->digit_bits, p->nbins, p->nkeys, n, p->d_bin_start, p->col_bits);
     p->launches++;
     return cudaGetLastError();
   }
   build_kernel<<<grid_for(n + 1, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys,
                                                             nullptr,   // xs comes from the sort
                                                             p->d_bin_start, n, p->opts.d,
-                                                            p->nbins, p->ub_log2, p->nkeys);
+                                                            p->nbins, p->ub_log2, p->nkeys, p->col_bits);
   p->launches++;
   return cudaGetLastError();
 }

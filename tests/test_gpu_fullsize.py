@@ -34,6 +34,10 @@ def check_sort_properties(torch, plan, x_dev):
         c = torch.clamp(c, max=info.L - 1)
         key = key * info.bins_per_dim[t] + (c >> info.bin_log2[t])
     key = (torch.arange(n, device=x_dev.device) >> info.user_block_log2) * info.nbins + key
+    cb = int(info.key_col_bits)   # minor sort digit: the y column inside the bin (bnfft_info)
+    if info.d >= 2 and cb:
+        c1 = torch.clamp(torch.floor(x_dev[:, 1] * L).long() + info.L // 2, max=info.L - 1)
+        key = key * (1 << cb) + (c1 & ((1 << cb) - 1))
     ks = key[perm]
     assert bool(torch.all(ks[1:] >= ks[:-1]))
     same = ks[1:] == ks[:-1]

@@ -125,10 +125,15 @@ def test_bin_sort_bit_exact(bn, torch, cid, d, M, N):
     key = np.zeros(N, dtype=np.int64)
     for t in range(d):
         key = key * info.bins_per_dim[t] + (cells[:, t] >> info.bin_log2[t])
-    # sort key (user block, bin) as documented in include/bnfft.h (bnfft_info)
+    # sort key ((user block, bin), y column) as documented in include/bnfft.h (bnfft_info); offsets
+    # per (user block, bin)
     key = (np.arange(N, dtype=np.int64) >> info.user_block_log2) * info.nbins + key
     assert info.nkeys == (((N - 1) >> info.user_block_log2) + 1) * info.nbins
-    perm_ref, off_ref = O.stable_bin_sort(key, int(info.nkeys))
+    cb = int(info.key_col_bits)
+    if d >= 2 and cb:
+        key = key * (1 << cb) + (cells[:, 1] & ((1 << cb) - 1))
+    perm_ref, _ = O.stable_bin_sort(key, int(info.nkeys) << cb)
+    _, off_ref = O.stable_bin_sort(key >> cb, int(info.nkeys))
     perm = plan.perm().cpu().numpy().astype(np.int64)
     off = plan.bin_offsets().cpu().numpy().astype(np.int64)
     assert np.array_equal(perm, perm_ref)
