@@ -221,7 +221,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
   static_assert(sizeof(GatherParams<R>) < 32000, "kernel parameter limit");
   GatherParams<R> gp;
   memset(&gp, 0, sizeof(gp));
-  gp.xs = p->d_xs;
+  gp.xs = p->rec3 ? (const double*)p->d_rec_user : p->d_xs;   // rec3: user-order 16-B records
   gp.perm = p->d_perm;
   gp.grid = p->d_grid;
   gp.out = out;

@@ -9,8 +9,9 @@
 //
 //   * sort (row a1): the key of a node is its x-line bin (cells cx x [16 by, 16 by + 16) x
 //     [8 bz, 8 bz + 8), bins of 1 x 16 x 8 cells) with the y column c_y mod 16 as a minor digit, so
-//     an x-line's nodes arrive in column order; the keys kernel writes a 16-B record per node
-//     (u_x, u_y, u_z as float, column and z offset) that the last radix pass gathers (rec3);
+//     an x-line's nodes arrive in column order; the keys kernel writes a 16-B record per node in
+//     user order (u_x, u_y, u_z as float, column and z offset; rec3), read here through the
+//     permutation one batch ahead of use;
 //   * a CTA of 16 warps = two teams of 8; an item = the 8 x-lines cx = 8X..8X+7 of one (by, bz),
 //     warp w of a team contracts x-line 8X + w; items alternate between the teams and their grid
 //     neighbourhoods (15 x 23 x 18 complex64, zero outside I_L = reading A5 zero extension) are
@@ -109,18 +110,27 @@ __device__ __forceinline__ void g3y_produce(const GatherParams<float>& p, const 
         ::"r"(d), "l"(t), "r"(b), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 
+// Phase B, load part: the permutation entry and the keys kernel's 16-B user-order record (rec3) of
+// sorted node s0 + lane (issued one batch ahead: the random record read overlaps a batch of nodes).
+__device__ __forceinline__ void g3y_fetch(const GatherParams<float>& p, uint32_t s0, uint32_t e, int lane,
+                                          float4& c4, uint32_t& pj) {
+  const uint32_t i = s0 + (uint32_t)lane;
+  if (i < e) {
+    pj = __ldg(&p.perm[i]);
+    c4 = __ldg(reinterpret_cast<const float4*>(p.xs) + pj);
+  }
+}
+
 // Phase B: records of sorted nodes [s0, min(s0 + 32, e)) (lane k: node s0 + k; the sort key's minor
 // digit puts an x-line's nodes in y-column order): the 24 tap weights (tap polynomials, R1), the y
 // weights as the pairs each row-lane group needs at the node's column, (column, z offset) and the
-// destination.  Reads the keys kernel's sorted 16-B records (rec3), coalesced.
+// destination.
 template <bool POLY>
 __device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32_t s0, uint32_t e, float* rec,
-                                            int lane) {
+                                            int lane, const float4 c4, const uint32_t pj) {
   constexpr int T = g3y::T;
   const uint32_t i = s0 + (uint32_t)lane;
   if (i < e) {
-    const float4 c4 = __ldg(reinterpret_cast<const float4*>(p.xs) + i);
-    const uint32_t pj = __ldg(&p.perm[i]);
     const uint32_t md = __float_as_uint(c4.w);
     const int col = (int)(md >> 3);
     float* r = rec + lane * g3y::REC;
@@ -248,7 +258,12 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
     }
     const float2* box = boxes + (size_t)b * (BOXB / 8);
     const int xa = wt + la;          // box x index of the lane's rows
-    if (nb0 < ne) g3y_phase_b<POLY>(p, nb0, ne, rec, lane);   // overlaps the box's TMA
+    float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t pj = 0;
+    if (nb0 < ne) {   // overlaps the box's TMA
+      g3y_fetch(p, nb0, ne, lane, c4, pj);
+      g3y_phase_b<POLY>(p, nb0, ne, rec, lane, c4, pj);
+    }
     while (s_tag[b] != (int)k) {
     }
     g3y_wait(&full[b], (k / NBUF) & 1u);
@@ -260,6 +275,7 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
       g3y_load_row(box, xa, ycur + ((lq + 4 - ycur) & 7), R1);
       for (uint32_t s0 = nb0;;) {
         const int nq = (int)min(32u, ne - s0);
+        if (s0 + 32 < ne) g3y_fetch(p, s0 + 32, ne, lane, c4, pj);   // next batch, in flight meanwhile
         float* r = rec;
         for (int q = 0; q < nq; ++q, r += REC) {
           const uint32_t md = reinterpret_cast<const uint32_t*>(r)[24];
@@ -319,7 +335,7 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
         __syncwarp();   // records free for the next batch
         s0 += 32;
         if (s0 >= ne) break;
-        g3y_phase_b<POLY>(p, s0, ne, rec, lane);
+        g3y_phase_b<POLY>(p, s0, ne, rec, lane, c4, pj);
       }
     }
     // ---- release box buffer b; the team's last warp loads item k + NBUF into it

@@ -758,12 +758,12 @@ cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n) {
       cudaError_t e = exclusive_scan(p, p->d_hist, p->d_hist, nh);
       if (e != cudaSuccess) return e;
       const bool last = pass == p->sort_passes - 1;
-      // last pass: the sorted copy of the per-node payload -- x (d doubles), or the rec3 record
-      // (16 B = two doubles, gathered from the keys kernel's user-order records)
+      // last pass: the sorted node copy xs (d doubles per node); none for rec3 plans, whose gather
+      // reads the keys kernel's user-order records through the permutation (those random reads
+      // overlap the gather's arithmetic instead of costing a bandwidth-bound pass here)
       scatter_for(b)<<<(unsigned)sl.ntiles, kSortThreads, 2 * kSortTile * sizeof(uint32_t), p->stream>>>(
-          kin, vin, (last && p->sort_passes == 1) ? nullptr : kout, vout, n, shift, p->d_hist, sl,
-          p->rec3 ? (const double*)p->d_rec_user : x, (last && !p->xs_user) ? p->d_xs : nullptr,
-          p->rec3 ? 2 : p->opts.d);
+          kin, vin, (last && p->sort_passes == 1) ? nullptr : kout, vout, n, shift, p->d_hist, sl, x,
+          (last && !p->xs_user && !p->rec3) ? p->d_xs : nullptr, p->opts.d);
       p->launches++;
       std::swap(kin, kout);
       if (!vin) {
