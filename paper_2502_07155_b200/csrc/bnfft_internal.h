@@ -109,6 +109,13 @@ struct bnfft_plan_s {
   void* d_grid = nullptr;       // batch x L^d complex, theta (centred)
   cufftHandle fft = 0;
   bool fft_ok = false;
+  // pruned step 2 (d = 3, batch 1, 2M <= L): the FFT input is zero outside I_M, so 2-D inverse FFTs
+  // over (k_2, k_3) run only on the M nonzero k_1 planes (compact buffer d_fft_p, two affine batches:
+  // k_1 >= 0 and k_1 < 0), into the nonzero planes of d_fft_in, then 1-D FFTs along k_1 (stride L^2)
+  bool pfft3 = false;
+  void* d_fft_p = nullptr;       // M x L x L complex: plane (k_1 mod M), rows k_2 mod L, k_3 mod L
+  cufftHandle fft2 = 0;
+  bool fft2_ok = false;
   double flatness = 0;
 
   // nodes

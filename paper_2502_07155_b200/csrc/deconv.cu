@@ -8,10 +8,12 @@
 
 namespace bnfft {
 
+// L0: modulus of the first index (L; M for the pruned 3-D transform's compact plane buffer, whose
+// plane k_1 mod M holds k_1 in I_M).
 template <typename C, typename R>
 __global__ void deconv_kernel(const C* __restrict__ fhat, C* __restrict__ X,
                               const double* __restrict__ q, int d, int64_t M, int64_t L,
-                              int64_t Md, int64_t Ld, int64_t total) {
+                              int64_t Md, int64_t Ld, int64_t total, int64_t L0) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     int64_t b = idx / Md;
@@ -26,7 +28,7 @@ __global__ void deconv_kernel(const C* __restrict__ fhat, C* __restrict__ X,
     for (int t = 0; t < d; ++t) {
       qq *= q[it[t]];
       int64_t k = it[t] - M / 2;
-      int64_t pk = k < 0 ? k + L : k;
+      int64_t pk = k < 0 ? k + (t == 0 ? L0 : L) : k;
       flat = flat * L + pk;
     }
     C v = fhat[idx];
@@ -41,14 +43,16 @@ cudaError_t launch_deconv(bnfft_plan_s* p, const void* fhat) {
   int64_t total = p->Md * p->opts.batch;
   if (total == 0) return cudaSuccess;
   int64_t blocks = std::min<int64_t>((total + 255) / 256, 148LL * 32);
+  void* X = p->pfft3 ? p->d_fft_p : p->d_fft_in;
+  const int64_t L0 = p->pfft3 ? p->opts.M : p->L;
   if (p->c128)
     deconv_kernel<double2, double><<<(unsigned)blocks, 256, 0, p->stream>>>(
-        (const double2*)fhat, (double2*)p->d_fft_in, p->d_q, p->opts.d, p->opts.M, p->L, p->Md,
-        p->Ld, total);
+        (const double2*)fhat, (double2*)X, p->d_q, p->opts.d, p->opts.M, p->L, p->Md,
+        p->Ld, total, L0);
   else
     deconv_kernel<float2, float><<<(unsigned)blocks, 256, 0, p->stream>>>(
-        (const float2*)fhat, (float2*)p->d_fft_in, p->d_q, p->opts.d, p->opts.M, p->L, p->Md,
-        p->Ld, total);
+        (const float2*)fhat, (float2*)X, p->d_q, p->opts.d, p->opts.M, p->L, p->Md,
+        p->Ld, total, L0);
   p->launches++;
   return cudaGetLastError();
 }

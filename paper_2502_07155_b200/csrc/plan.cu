@@ -196,7 +196,9 @@ int bnfft_destroy(bnfft_plan_s* p) {
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_pre) cudaEventDestroy(p->ev_pre);
   if (p->fft_ok) cufftDestroy(p->fft);
+  if (p->fft2_ok) cufftDestroy(p->fft2);
   dist_destroy(p);
+  dfree_plan(p, p->d_fft_p);
   dfree_plan(p, p->d_gl);
   dfree_plan(p, p->d_psihat);
   dfree_plan(p, p->d_q);
@@ -422,6 +424,12 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     CK(dmalloc(p, &p->d_bad, sizeof(unsigned long long)), "alloc status");
     CK(cudaMallocHost((void**)&p->h_bad, sizeof(unsigned long long)), "alloc pinned status");
     if (!slab) CK(cudaMemsetAsync(p->d_fft_in, 0, gbytes, p->stream), "zero fft input");
+    p->pfft3 = !slab && o->d == 3 && o->batch == 1 && 2 * o->M <= L && !getenv("BNFFT_NO_PFFT");
+    if (p->pfft3) {
+      const size_t pb = (size_t)o->M * L * L * p->csize;
+      CK(dmalloc(p, &p->d_fft_p, pb), "alloc pruned fft planes");
+      CK(cudaMemsetAsync(p->d_fft_p, 0, pb, p->stream), "zero pruned fft planes");
+    }
     CK(cudaMemsetAsync(p->d_grid, 0, gbytes, p->stream), "zero grid");
     double th[2 * kQuadN];
     gauss_legendre_theta(kQuadN, th, th + kQuadN);
@@ -459,12 +467,33 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
     int n[3] = {(int)L, (int)L, (int)L};
     size_t ws = 0;
     cufftResult fr = CUFFT_SUCCESS;
-    if (!slab) {
+    if (!slab && !p->pfft3) {
       fr = cufftCreate(&p->fft);
       if (fr == CUFFT_SUCCESS) {
         p->fft_ok = true;
         fr = cufftMakePlanMany(p->fft, o->d, n, nullptr, 1, (int)Ld, nullptr, 1, (int)Ld,
                                p->c128 ? CUFFT_Z2Z : CUFFT_C2C, o->batch, &ws);
+      }
+      if (fr == CUFFT_SUCCESS) fr = cufftSetStream(p->fft, p->stream);
+    } else if (p->pfft3) {
+      // step 2 pruned (d = 3): 2-D FFTs over (k_2, k_3) on M/2 compact planes per call, then 1-D FFTs
+      // along k_1 with stride L^2 over all L^2 lines
+      const cufftType ty = p->c128 ? CUFFT_Z2Z : CUFFT_C2C;
+      fr = cufftCreate(&p->fft2);
+      if (fr == CUFFT_SUCCESS) {
+        p->fft2_ok = true;
+        int n2[2] = {(int)L, (int)L};
+        fr = cufftMakePlanMany(p->fft2, 2, n2, nullptr, 1, (int)(L * L), nullptr, 1, (int)(L * L), ty,
+                               (int)(o->M / 2), &ws);
+        p->device_bytes += (int64_t)ws;
+      }
+      if (fr == CUFFT_SUCCESS) fr = cufftSetStream(p->fft2, p->stream);
+      if (fr == CUFFT_SUCCESS) fr = cufftCreate(&p->fft);
+      if (fr == CUFFT_SUCCESS) {
+        p->fft_ok = true;
+        int n1[1] = {(int)L};
+        int nem[1] = {(int)L};
+        fr = cufftMakePlanMany(p->fft, 1, n1, nem, (int)(L * L), 1, nem, (int)(L * L), 1, ty, (int)(L * L), &ws);
       }
       if (fr == CUFFT_SUCCESS) fr = cufftSetStream(p->fft, p->stream);
     }
@@ -630,10 +659,21 @@ int bnfft_execute(bnfft_plan_s* p, const void* fhat, void* f) {
   if ((e = launch_deconv(p, fhat)) != cudaSuccess) return cuda_fail(e, "deconv kernel");
   timer_end(p, ST_DECONV, ev);
   timer_begin(p, ST_FFT, &ev);
-  cufftResult fr = p->c128 ? cufftExecZ2Z(p->fft, (cufftDoubleComplex*)p->d_fft_in,
-                                          (cufftDoubleComplex*)p->d_grid, CUFFT_INVERSE)
-                           : cufftExecC2C(p->fft, (cufftComplex*)p->d_fft_in,
-                                          (cufftComplex*)p->d_grid, CUFFT_INVERSE);
+  cufftResult fr = CUFFT_SUCCESS;
+  if (p->pfft3) {   // planes k_1 in [0, M/2) -> [0, M/2), k_1 in [-M/2, 0) -> [L - M/2, L)
+    const size_t pl = (size_t)p->L * p->L, half = (size_t)(p->opts.M / 2);
+    for (int h = 0; h < 2 && fr == CUFFT_SUCCESS; ++h) {
+      const size_t src = h * half * pl, dst = (h ? (size_t)p->L - half : 0) * pl;
+      fr = p->c128 ? cufftExecZ2Z(p->fft2, (cufftDoubleComplex*)p->d_fft_p + src,
+                                  (cufftDoubleComplex*)p->d_fft_in + dst, CUFFT_INVERSE)
+                   : cufftExecC2C(p->fft2, (cufftComplex*)p->d_fft_p + src, (cufftComplex*)p->d_fft_in + dst,
+                                  CUFFT_INVERSE);
+    }
+  }
+  if (fr == CUFFT_SUCCESS)
+    fr = p->c128 ? cufftExecZ2Z(p->fft, (cufftDoubleComplex*)p->d_fft_in, (cufftDoubleComplex*)p->d_grid,
+                                CUFFT_INVERSE)
+                 : cufftExecC2C(p->fft, (cufftComplex*)p->d_fft_in, (cufftComplex*)p->d_grid, CUFFT_INVERSE);
   if (fr != CUFFT_SUCCESS) {
     char buf[64];
     snprintf(buf, sizeof(buf), "cufftExec failed (%d)", (int)fr);
