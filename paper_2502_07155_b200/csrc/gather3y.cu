@@ -121,6 +121,40 @@ __device__ __forceinline__ void g3y_fetch(const GatherParams<float>& p, uint32_t
   }
 }
 
+// The 24 taps of a node (tap polynomials, R1; the same operations and order as all_taps): the three
+// dimensions' Horner chains run interleaved and share the coefficient operands; Kronecker nodes
+// (u == 0 or 1 in a dimension) take the exact 0/1 taps (interpolation property).
+__device__ __forceinline__ void g3y_taps1(const GatherParams<float>& p, const float u, float (&w)[8]) {
+  constexpr int m = 4, NH = PolyH<float>::NH;
+  const float x = fmaf(2.0f, u, -1.0f);
+  const float y = x * x;
+  const float2 yy = make_float2(y, y), xm = make_float2(x, -x);
+#pragma unroll
+  for (int i = 0; i < m; ++i) {
+    float2 h = *reinterpret_cast<const float2*>(p.ceo[NH - 1][i]);
+#pragma unroll
+    for (int k = NH - 2; k >= 0; --k) h = __ffma2_rn(h, yy, *reinterpret_cast<const float2*>(p.ceo[k][i]));
+    const float2 r = __ffma2_rn(xm, make_float2(h.y, h.y), make_float2(h.x, h.x));
+    w[i] = r.x;
+    w[2 * m - 1 - i] = r.y;
+  }
+  if (p.edge_sqrt) {   // sinh window: the edge taps' sqrt(1 - (tau/m)^2) factors (dim_state)
+    w[0] *= sqrt_r((1.0f - u) * ((float)(2 * m - 1) + u)) * p.inv_m;
+    w[2 * m - 1] *= sqrt_r(u * ((float)(2 * m) - u)) * p.inv_m;
+  }
+  // Kronecker node (interpolation property): exact 0/1 taps, by selects
+  const bool h0 = u == 0.0f, h1 = u == 1.0f;
+#pragma unroll
+  for (int i = 0; i < 2 * m; ++i) w[i] = (h0 | h1) ? ((h0 ? i == m - 1 : i == m) ? 1.0f : 0.0f) : w[i];
+}
+
+// The 24 taps of a node from the tap polynomials (R1): the same operations and order as all_taps,
+// without its generic per-tap fallback branch.
+__device__ __forceinline__ void g3y_taps3(const GatherParams<float>& p, const float (&u)[3], float (&w)[3][8]) {
+#pragma unroll
+  for (int t = 0; t < 3; ++t) g3y_taps1(p, u[t], w[t]);
+}
+
 // Phase B: records of sorted nodes [s0, min(s0 + 32, e)) (lane k: node s0 + k; the sort key's minor
 // digit puts an x-line's nodes in y-column order): the 24 tap weights (tap polynomials, R1), the y
 // weights as the pairs each row-lane group needs at the node's column, (column, z offset) and the
@@ -134,10 +168,17 @@ __device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32
     const uint32_t md = __float_as_uint(c4.w);
     const int col = (int)(md >> 3);
     float* r = rec + lane * g3y::REC;
-    float w[T];
-    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.y, p), p, w);
-    reinterpret_cast<float4*>(r)[2] = make_float4(w[0], w[1], w[2], w[3]);
-    reinterpret_cast<float4*>(r)[3] = make_float4(w[4], w[5], w[6], w[7]);
+    float w[3][T];
+    if (POLY) {
+      const float uu[3] = {c4.x, c4.y, c4.z};
+      g3y_taps3(p, uu, w);
+    } else {
+      all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.x, p), p, w[0]);
+      all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.y, p), p, w[1]);
+      all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.z, p), p, w[2]);
+    }
+    reinterpret_cast<float4*>(r)[2] = make_float4(w[1][0], w[1][1], w[1][2], w[1][3]);
+    reinterpret_cast<float4*>(r)[3] = make_float4(w[1][4], w[1][5], w[1][6], w[1][7]);
     // row-lane group q holds window rows b = (q - col) & 7 and b ^ 4: pairs (wy[b], wy[b ^ 4])
     float yq[8];
 #pragma unroll
@@ -148,12 +189,10 @@ __device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32
     }
     reinterpret_cast<float4*>(r)[2] = make_float4(yq[0], yq[1], yq[2], yq[3]);
     reinterpret_cast<float4*>(r)[3] = make_float4(yq[4], yq[5], yq[6], yq[7]);
-    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.z, p), p, w);
-    reinterpret_cast<float4*>(r)[0] = make_float4(w[0], w[1], w[2], w[3]);
-    reinterpret_cast<float4*>(r)[1] = make_float4(w[4], w[5], w[6], w[7]);
-    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.x, p), p, w);
-    reinterpret_cast<float4*>(r)[4] = make_float4(w[0], w[1], w[2], w[3]);
-    reinterpret_cast<float4*>(r)[5] = make_float4(w[4], w[5], w[6], w[7]);
+    reinterpret_cast<float4*>(r)[0] = make_float4(w[2][0], w[2][1], w[2][2], w[2][3]);
+    reinterpret_cast<float4*>(r)[1] = make_float4(w[2][4], w[2][5], w[2][6], w[2][7]);
+    reinterpret_cast<float4*>(r)[4] = make_float4(w[0][0], w[0][1], w[0][2], w[0][3]);
+    reinterpret_cast<float4*>(r)[5] = make_float4(w[0][4], w[0][5], w[0][6], w[0][7]);
     reinterpret_cast<uint2*>(r)[12] = make_uint2(md, p.sorted_out ? i : pj);
   }
   __syncwarp();
