@@ -84,9 +84,13 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   int bt = (int)std::max<size_t>(1, std::min<size_t>((size_t)p->opts.batch, budget / per));
   if (bt > 256) bt = 256;
   const size_t buf_bytes = (per * bt + 127) & ~(size_t)127;
-  // coop kernel: one box buffer, more CTAs per SM; gatherN: three buffers when they fit 100 KB
-  // (mbarrier-released, see gatherN_kernel), else two
-  const int nbuf = use_coop3(p) ? 1 : (3 * buf_bytes <= ((size_t)100 << 10) ? 3 : 2);
+  // coop kernel: one box buffer, more CTAs per SM; gatherN: a ring of up to kMaxBoxBufs buffers
+  // (mbarrier-released, see gatherN_kernel) within 100 KB (at least two)
+  int nbuf = 1;
+  if (!use_coop3(p)) {
+    nbuf = 3 * buf_bytes <= ((size_t)100 << 10) ? 3 : 2;
+    if (const char* s = getenv("BNFFT_BOX_BUFS")) nbuf = std::max(2, std::min(kMaxBoxBufs, atoi(s)));   // tuning knob
+  }
   p->gather_nbuf = nbuf;
   p->gather_bt = bt;
   p->gather_nslice = (p->opts.batch + bt - 1) / bt;
@@ -95,6 +99,10 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   for (int t = 0; t < 3; ++t) p->gather_tbox[t] = t < d ? ext[t] : 1;
   p->gather_smem = use_sweep3(p) ? gather3s_smem() : use_ysweep3(p) ? gather3y_smem() : nbuf * buf_bytes;
   p->gather_threads = use_sweep3(p) ? gather3s_threads() : use_ysweep3(p) ? gather3y_threads() : kGatherThreads;
+  // tuning knob: 128-thread box CTAs (measured equal to 256 on cfg3: the kernel is latency-bound on
+  // the node loads and box hand-offs, not on idle threads of sparse bins)
+  if (!use_coop3(p))
+    if (const char* s = getenv("BNFFT_GATHERN_THREADS")) p->gather_threads = atoi(s) == 128 ? 128 : 256;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0, nsm = 0, dev = 0;

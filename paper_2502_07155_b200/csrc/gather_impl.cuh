@@ -835,13 +835,17 @@ __device__ __forceinline__ void issue_box(const GatherParams<R>& p, const CUtens
   tma_load_box(tm, dst, bar, r, c);
 }
 
+constexpr int kMaxBoxBufs = 6;
+
 template <int D, int T, typename R, bool POLY>
 __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_constant__ GatherParams<R> p,
                                                                  const CUtensorMap* __restrict__ tmap) {
   using C = typename CT<R>::C;
   constexpr int m = T / 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[3], empty[3];
+  __shared__ __align__(8) uint64_t full[kMaxBoxBufs], empty[kMaxBoxBufs];
+  __shared__ int64_t s_u[kMaxBoxBufs];   // item (key) staged in each buffer, -1: end of the CTA's items
+  __shared__ int s_sl[kMaxBoxBufs];
   const int BZ = p.tbox[D - 1];                      // innermost (padded) extent
   const int BY = D == 3 ? p.tbox[1] : 1;
   const int box_elems = p.box_elems;                 // per spectrum (with padding)
@@ -851,58 +855,53 @@ __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_co
   const int64_t G = gridDim.x;
   const int nsl = p.nslice;
   const int NB = p.nbuf;
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < NB; ++q) {
-      mbar_init(&full[q], 1);
-      mbar_init(&empty[q], kGatherThreads);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
   C* __restrict__ out = (C*)p.out;
 
-  // the CTA's item sequence: keys u = blockIdx.x + j*G (non-empty ones), slices 0..nsl-1 each.
-  // Item i uses buffer i % NB; thread 0 issues item i+NB-1 once every thread released item i-1, so
-  // threads that finish an item early move on to the next (already staged) one instead of waiting.
+  // The CTA's item sequence: keys u = blockIdx.x + j*G (non-empty ones), slices 0..nsl-1 each.
+  // Item i uses buffer i % NB.  Thread 0 walks the sequence and stages item i + NB - 1 (descriptor in
+  // s_u / s_sl, box by TMA) once every thread has released item i - 1, the previous user of that
+  // buffer; so NB - 1 boxes are in flight while an item is contracted (small items: deep ring).
+  int64_t wu = blockIdx.x;   // thread 0's walk position
+  int wsl = 0;
   auto next_key = [&](int64_t u) -> int64_t {
     while (u < p.nkeys && __ldg(&p.key_start[u + 1]) == __ldg(&p.key_start[u])) u += G;
     return u;
   };
-  auto advance = [&](int64_t& u, int& sl) {
-    if (u >= p.nkeys) return;
-    if (++sl == nsl) {
-      sl = 0;
-      u = next_key(u + G);
+  auto stage = [&](int bq) {   // thread 0: the next item of the walk into buffer bq (or the end mark)
+    if (wu < p.nkeys) {
+      s_u[bq] = wu;
+      s_sl[bq] = wsl;
+      issue_box<D, R>(p, tmap, wu, wsl, buf0 + bq * p.bufstride, &full[bq], bytes);
+      if (++wsl == nsl) {
+        wsl = 0;
+        wu = next_key(wu + G);
+      }
+    } else {
+      s_u[bq] = -1;
+      mbar_arrive(&full[bq]);   // completes the phase: waiters read the end mark
     }
   };
-  int64_t u = next_key(blockIdx.x);
-  int sl = 0;
-  if (u >= p.nkeys) return;
-  // look-ahead items (NB - 1 ahead at most 2)
-  int64_t u1 = u, u2;
-  int s1 = sl, s2;
-  advance(u1, s1);
-  u2 = u1;
-  s2 = s1;
-  advance(u2, s2);
   if (threadIdx.x == 0) {
-    issue_box<D, R>(p, tmap, u, sl, buf0, &full[0], bytes);
-    if (NB == 3 && u1 < p.nkeys) issue_box<D, R>(p, tmap, u1, s1, buf0 + p.bufstride, &full[1], bytes);
+    for (int q = 0; q < NB; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], blockDim.x);
+    }
+    fence_mbar_init();
+    wu = next_key(wu);
+    for (int q = 0; q < NB - 1; ++q) stage(q);
   }
-  uint32_t phases = 0u;
+  __syncthreads();
   for (int it = 0;; ++it) {
     const int b = it % NB;
     if (threadIdx.x == 0) {
-      const int64_t ua = NB == 3 ? u2 : u1;
-      const int sa = NB == 3 ? s2 : s1;
-      if (ua < p.nkeys) {
-        const int bn = (it + NB - 1) % NB;
-        if (it >= 1 && NB == 3) mbar_wait(&empty[bn], (uint32_t)((it - 1) / NB) & 1u);
-        issue_box<D, R>(p, tmap, ua, sa, buf0 + bn * p.bufstride, &full[bn], bytes);
-      }
+      const int bn = (it + NB - 1) % NB;
+      if (it >= 1 && NB > 2) mbar_wait(&empty[bn], (uint32_t)((it - 1) / NB) & 1u);
+      stage(bn);   // NB == 2: the CTA barrier at the end of item it-1 released the buffer
     }
-    mbar_wait(&full[b], (phases >> b) & 1u);
-    phases ^= 1u << b;
+    mbar_wait(&full[b], (uint32_t)(it / NB) & 1u);
+    const int64_t u = s_u[b];
+    if (u < 0) break;
+    const int sl = s_sl[b];
     const C* box = buf0 + b * p.bufstride;
     // bin origin (cells) of key u
     int64_t nbins = 1;
@@ -918,7 +917,7 @@ __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_co
     }
     const int64_t i_beg = __ldg(&p.key_start[u]), i_end = __ldg(&p.key_start[u + 1]);
     const int nbt = min(p.bt, p.batch - sl * p.bt);
-    for (int64_t i = i_beg + threadIdx.x; i < i_end; i += kGatherThreads) {
+    for (int64_t i = i_beg + threadIdx.x; i < i_end; i += blockDim.x) {
       const uint32_t dst = __ldg(&p.perm[i]);
       const int64_t src = p.xs_user ? (int64_t)dst : i;
       int off[3];
@@ -969,16 +968,10 @@ __global__ void __launch_bounds__(kGatherThreads) gatherN_kernel(const __grid_co
         out[(int64_t)(sl * p.bt + bb) * p.n + (p.sorted_out ? i : (int64_t)dst)] = acc;
       }
     }
-    if (u1 >= p.nkeys) break;
-    // buffer b is refilled NB-1 items later: three buffers hand it back per thread (mbarrier), two
-    // (large batched boxes) with a CTA barrier, which measured faster there (cfg5)
-    if (NB == 3) mbar_arrive(&empty[b]);
+    // buffer b is refilled NB-1 items later: handed back per thread by mbarrier, or (two large
+    // batched boxes) by a CTA barrier, which measured faster there (cfg5)
+    if (NB > 2) mbar_arrive(&empty[b]);
     else __syncthreads();
-    u = u1;
-    sl = s1;
-    u1 = u2;
-    s1 = s2;
-    advance(u2, s2);
   }
 }
 
