@@ -236,6 +236,19 @@ BNFFT_API int bnfft_kernel_hat(struct bnfft_plan_s* plan, int64_t n, const doubl
 BNFFT_API int bnfft_transform_host(struct bnfft_plan_s* plan, int64_t n, const double* x_host,
                          const void* fhat_host, void* f_host, int64_t* first_bad);
 
+/* Pipelined end-to-end transforms with HOST buffers: `steps` complete runs of Algorithm 2 (step 0(a),
+ * set_nodes, execute) on node sets of n nodes each: step k reads x_host[k] (n x d float64, user order)
+ * and fhat_host[k], and writes f_host[k] (layouts as bnfft_execute).  Step k+1's host->device copies,
+ * step k's compute and step k-1's device->host copy run on three streams and overlap (two device
+ * staging slots, owned by the plan); host buffers must be pinned for the copies to overlap.  Different
+ * steps may share input buffers; output buffers of consecutive steps must differ.  Synchronous: returns
+ * after the last copy.  A step with an invalid node returns that node's code (first_bad = its index in
+ * that step's node set; bnfft_last_error names the step); outputs of that step are undefined.
+ * Multi-rank plans run the steps one by one. */
+BNFFT_API int bnfft_transform_host_many(struct bnfft_plan_s* plan, int32_t steps, int64_t n,
+                                        const double* const* x_host, const void* const* fhat_host,
+                                        void* const* f_host, int64_t* first_bad);
+
 BNFFT_API int bnfft_get_info(const struct bnfft_plan_s* plan, bnfft_info* out);
 BNFFT_API int bnfft_get_timing(struct bnfft_plan_s* plan, bnfft_timing* out);
 BNFFT_API int bnfft_reset_timing(struct bnfft_plan_s* plan);

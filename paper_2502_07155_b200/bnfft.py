@@ -91,6 +91,8 @@ _sig = {
     "bnfft_set_nodes": (c_int, [_P, c_int64, c_void_p, POINTER(c_int64)]),
     "bnfft_execute": (c_int, [_P, c_void_p, c_void_p]),
     "bnfft_transform_host": (c_int, [_P, c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_int64)]),
+    "bnfft_transform_host_many": (c_int, [_P, c_int32, c_int64, POINTER(c_void_p), POINTER(c_void_p),
+                                          POINTER(c_void_p), POINTER(c_int64)]),
     "bnfft_interpolate": (c_int, [_P, c_void_p, c_void_p]),
     "bnfft_kernel_hat": (c_int, [_P, c_int64, c_void_p, c_void_p]),
     "bnfft_get_info": (c_int, [_P, POINTER(bnfft_info)]),
@@ -225,6 +227,21 @@ class Plan:
         bad = c_int64(-1)
         check(bnfft_transform_host(self.h, x_host.shape[0], _ptr(x_host), _ptr(fhat_host),
                                    _ptr(f_host), ctypes.byref(bad)), "bnfft_transform_host")
+
+    def transform_host_many(self, xs, fhats, fs) -> None:
+        """Pipelined host transforms (bnfft_transform_host_many): step k reads xs[k], fhats[k] and
+        writes fs[k] (pinned host tensors; consecutive outputs must be distinct buffers)."""
+        k = len(xs)
+        assert len(fhats) == k and len(fs) == k
+        n = xs[0].shape[0] if k else 0
+        arr = c_void_p * max(k, 1)
+        bad = c_int64(-1)
+        code = bnfft_transform_host_many(self.h, k, n, arr(*[_ptr(t) for t in xs]), arr(*[_ptr(t) for t in fhats]),
+                                         arr(*[_ptr(t) for t in fs]), ctypes.byref(bad))
+        if code != BNFFT_OK:
+            err = BnfftError(code, "bnfft_transform_host_many")
+            err.first_bad = bad.value
+            raise err
 
     def info(self) -> bnfft_info:
         i = bnfft_info()

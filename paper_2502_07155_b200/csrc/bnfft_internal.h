@@ -143,6 +143,15 @@ struct bnfft_plan_s {
   double* d_x_stage = nullptr; int64_t x_stage_cap = 0;
   void* d_fhat_stage = nullptr;
   void* d_f_stage = nullptr; int64_t f_stage_cap = 0;
+  // pipelined host transforms (bnfft_transform_host_many): two staging slots, copy streams, events
+  double* d_xp[2] = {nullptr, nullptr};
+  void* d_fhp[2] = {nullptr, nullptr};
+  void* d_fp[2] = {nullptr, nullptr};
+  int64_t pipe_cap = -1;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr}, ev_f[2] = {nullptr, nullptr},
+              ev_d2h[2] = {nullptr, nullptr};
+  unsigned long long* h_bads = nullptr; int32_t h_bads_cap = 0;
 
   int gather_bt = 1;          // batch slice per staged box
   int gather_smax = 1;        // segments (bins) staged per round
@@ -207,7 +216,10 @@ void dist_destroy(bnfft_plan_s* p);
 int dist_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad);
 int dist_execute(bnfft_plan_s* p, const void* fhat, void* f);
 void dist_fill_info(const bnfft_plan_s* p, bnfft_info* o);
-int local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad);   // single-rank body
+// single-rank body of bnfft_set_nodes; with h_bad_dst the validation word is copied there
+// asynchronously and the call returns without synchronizing (pipelined host transforms)
+int local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad,
+                    unsigned long long* h_bad_dst = nullptr);
 cudaError_t launch_deconv_slab(bnfft_plan_s* p, const void* fhat, void* out, int64_t k0_lo, int64_t k0_hi);
 
 }  // namespace bnfft

@@ -212,6 +212,16 @@ int bnfft_destroy(bnfft_plan_s* p) {
   dfree_plan(p, p->d_x_stage);
   dfree_plan(p, p->d_fhat_stage);
   dfree_plan(p, p->d_f_stage);
+  for (int k = 0; k < 2; ++k) {
+    dfree_plan(p, p->d_xp[k]);
+    dfree_plan(p, p->d_fhp[k]);
+    dfree_plan(p, p->d_fp[k]);
+    for (cudaEvent_t ev : {p->ev_h2d[k], p->ev_used[k], p->ev_f[k], p->ev_d2h[k]})
+      if (ev) cudaEventDestroy(ev);
+  }
+  if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+  if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+  if (p->h_bads) cudaFreeHost(p->h_bads);
   dfree_plan(p, p->d_tmap);
   dfree_plan(p, p->d_pre_w);
   free_nodes(p);
@@ -548,7 +558,8 @@ int bnfft_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_
 }  // extern "C"
 
 // the one-rank body of bnfft_set_nodes (also the owner-side step of BNFFT_DIST_SLAB)
-int bnfft::local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad) {
+int bnfft::local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_bad,
+                           unsigned long long* h_bad_dst) {
   if (first_bad) *first_bad = -1;
   p->nodes_set = false;
   cudaError_t e;
@@ -594,8 +605,8 @@ int bnfft::local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t*
   timer_begin(p, ST_KEYS, &ev);
   if ((e = launch_keys(p, x, n)) != cudaSuccess) return cuda_fail(e, "keys kernel");
   timer_end(p, ST_KEYS, ev);
-  if ((e = cudaMemcpyAsync(p->h_bad, p->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                           p->stream)) != cudaSuccess)
+  if ((e = cudaMemcpyAsync(h_bad_dst ? h_bad_dst : p->h_bad, p->d_bad, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, p->stream)) != cudaSuccess)
     return cuda_fail(e, "status copy");
   timer_begin(p, ST_SORT, &ev);
   if ((e = launch_sort(p, x, n)) != cudaSuccess) return cuda_fail(e, "sort kernels");
@@ -622,6 +633,12 @@ int bnfft::local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t*
     if ((e = launch_build(p, x, n)) != cudaSuccess) return cuda_fail(e, "build kernel");
     timer_end(p, ST_BUILD, ev);
     p->offsets_valid = true;
+  }
+  if (h_bad_dst) {   // pipelined: the caller checks the validation word after synchronizing
+    p->n = n;
+    p->nodes_set = true;
+    p->n_set++;
+    return BNFFT_OK;
   }
   if ((e = cudaStreamSynchronize(p->stream)) != cudaSuccess) return cuda_fail(e, "set_nodes sync");
   unsigned long long bad = *p->h_bad;
@@ -750,6 +767,103 @@ int bnfft_transform_host(bnfft_plan_s* p, int64_t n, const double* x_host, const
   if (n > 0 && (e = cudaMemcpyAsync(f_host, p->d_f_stage, fb, cudaMemcpyDeviceToHost, p->stream)) != cudaSuccess)
     return cuda_fail(e, "D2H f");
   if ((e = cudaStreamSynchronize(p->stream)) != cudaSuccess) return cuda_fail(e, "transform sync");
+  return BNFFT_OK;
+}
+
+int bnfft_transform_host_many(bnfft_plan_s* p, int32_t steps, int64_t n, const double* const* x_host,
+                              const void* const* fhat_host, void* const* f_host, int64_t* first_bad) {
+  if (first_bad) *first_bad = -1;
+  if (!p || steps < 0 || (steps > 0 && (!x_host || !fhat_host || !f_host))) return BNFFT_E_INVALID_ARG;
+  if (n < 0 || n >= ((int64_t)1 << 31)) return BNFFT_E_INVALID_ARG;
+  for (int k = 0; k < steps; ++k)
+    if (!fhat_host[k] || (n > 0 && (!x_host[k] || !f_host[k]))) return BNFFT_E_INVALID_ARG;
+  if (p->dist) {   // multi-rank plans: the collectives order the steps; run them one by one
+    for (int k = 0; k < steps; ++k) {
+      int rc = bnfft_precompute(p);
+      if (rc == BNFFT_OK) rc = bnfft_transform_host(p, n, x_host[k], fhat_host[k], f_host[k], first_bad);
+      if (rc != BNFFT_OK) return rc;
+    }
+    return BNFFT_OK;
+  }
+  cudaSetDevice(p->device);
+  cudaError_t e;
+  const size_t xb = (size_t)n * p->opts.d * sizeof(double);
+  const size_t fhb = (size_t)p->Md * p->opts.batch * p->csize;
+  const size_t fb = (size_t)n * p->opts.batch * p->csize;
+  if (!p->s_h2d) {
+    if ((e = cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "copy streams");
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t* ev : {&p->ev_h2d[k], &p->ev_used[k], &p->ev_f[k], &p->ev_d2h[k]})
+        if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "events");
+  }
+  if (n > p->pipe_cap) {
+    for (int k = 0; k < 2; ++k) {
+      dfree_plan(p, p->d_xp[k]);
+      dfree_plan(p, p->d_fhp[k]);
+      dfree_plan(p, p->d_fp[k]);
+      p->d_xp[k] = nullptr;
+      p->d_fhp[k] = p->d_fp[k] = nullptr;
+      if ((e = dmalloc(p, &p->d_xp[k], std::max<size_t>(xb, 16))) != cudaSuccess ||
+          (e = dmalloc(p, &p->d_fhp[k], fhb)) != cudaSuccess ||
+          (e = dmalloc(p, &p->d_fp[k], std::max<size_t>(fb, 16))) != cudaSuccess)
+        return cuda_fail(e, "alloc pipeline stages");
+    }
+    p->pipe_cap = n;
+  }
+  if (steps > p->h_bads_cap) {
+    if (p->h_bads) cudaFreeHost(p->h_bads);
+    p->h_bads = nullptr;
+    if ((e = cudaMallocHost((void**)&p->h_bads, (size_t)steps * sizeof(unsigned long long))) != cudaSuccess)
+      return cuda_fail(e, "alloc status ring");
+    p->h_bads_cap = steps;
+  }
+  for (int k = 0; k < steps; ++k) {
+    const int s = k & 1;
+    // inputs of step k into slot s once step k-2 is done reading it
+    if (k >= 2 && (e = cudaStreamWaitEvent(p->s_h2d, p->ev_used[s], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    if (n > 0 && (e = cudaMemcpyAsync(p->d_xp[s], x_host[k], xb, cudaMemcpyHostToDevice, p->s_h2d)) != cudaSuccess)
+      return cuda_fail(e, "H2D x");
+    if ((e = cudaMemcpyAsync(p->d_fhp[s], fhat_host[k], fhb, cudaMemcpyHostToDevice, p->s_h2d)) != cudaSuccess)
+      return cuda_fail(e, "H2D fhat");
+    if ((e = cudaEventRecord(p->ev_h2d[s], p->s_h2d)) != cudaSuccess) return cuda_fail(e, "record");
+    // compute on the plan's stream: step 0(a) (side stream), set_nodes, execute
+    if ((e = cudaStreamWaitEvent(p->stream, p->ev_h2d[s], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    if (k >= 2 && (e = cudaStreamWaitEvent(p->stream, p->ev_d2h[s], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    int rc = bnfft_precompute(p);
+    if (rc == BNFFT_OK) rc = local_set_nodes(p, n, p->d_xp[s], nullptr, &p->h_bads[k]);
+    if (rc == BNFFT_OK) rc = bnfft_execute(p, p->d_fhp[s], p->d_fp[s]);
+    if (rc != BNFFT_OK) {
+      cudaDeviceSynchronize();
+      return rc;
+    }
+    if ((e = cudaEventRecord(p->ev_used[s], p->stream)) != cudaSuccess ||
+        (e = cudaEventRecord(p->ev_f[s], p->stream)) != cudaSuccess)
+      return cuda_fail(e, "record");
+    // outputs of step k back while step k+1 runs
+    if ((e = cudaStreamWaitEvent(p->s_d2h, p->ev_f[s], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    if (n > 0 && (e = cudaMemcpyAsync(f_host[k], p->d_fp[s], fb, cudaMemcpyDeviceToHost, p->s_d2h)) != cudaSuccess)
+      return cuda_fail(e, "D2H f");
+    if ((e = cudaEventRecord(p->ev_d2h[s], p->s_d2h)) != cudaSuccess) return cuda_fail(e, "record");
+  }
+  if ((e = cudaStreamSynchronize(p->s_d2h)) != cudaSuccess || (e = cudaStreamSynchronize(p->stream)) != cudaSuccess)
+    return cuda_fail(e, "pipeline sync");
+  for (int k = 0; k < steps; ++k) {
+    const unsigned long long bad = p->h_bads[k];
+    if (bad == ~0ull) continue;
+    const int64_t idx = (int64_t)(bad >> 4);
+    const int code = (int)(bad & 15);
+    if (first_bad) *first_bad = idx;
+    char buf[128];
+    snprintf(buf, sizeof(buf), "step %d: node %lld rejected", k, (long long)idx);
+    set_error(buf);
+    p->n = 0;
+    p->nodes_set = false;
+    if (code == 1) return BNFFT_E_NODE_NOT_FINITE;
+    if (code == 2) return BNFFT_E_NODE_OUT_OF_RANGE;
+    return BNFFT_E_NODE_OUTSIDE_FEASIBLE_BOX;
+  }
   return BNFFT_OK;
 }
 

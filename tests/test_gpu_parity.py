@@ -222,6 +222,36 @@ def test_transform_host_matches_device(bn, torch):
     plan.close()
 
 
+@pytest.mark.parametrize("d,M,m,prec", [(1, 1 << 10, 8, "c64"), (3, 16, 4, "c64"), (2, 32, 5, "c128")])
+def test_transform_host_many_pipelined(bn, torch, d, M, m, prec):
+    """bnfft_transform_host_many: five steps with different node sets and spectra, each equal bitwise
+    to the device path (set_nodes + execute) on the same inputs; a bad node in one step is reported
+    with its step-local index."""
+    cid = {1: 2, 2: 3, 3: 4}[d]
+    cfg = synth.CONFIGS[cid].scaled(d=d, M=M, N=3001, batch=1)
+    K = 5
+    xs = [synth.make_nodes(cfg, variant=20 + k) for k in range(K)]
+    fhs = [synth.make_spectrum(cfg, variant=20 + k, prec=prec) for k in range(K)]
+    ct = torch.complex128 if prec == "c128" else torch.complex64
+    plan = bn.Plan(d, M, 2.0, m, "sinh", prec)
+    ref = []
+    for k in range(K):
+        plan.set_nodes(torch.from_numpy(xs[k]).cuda())
+        ref.append(plan.execute(torch.from_numpy(fhs[k]).cuda()).cpu().numpy())
+    xh = [torch.from_numpy(x).pin_memory() for x in xs]
+    fhh = [torch.from_numpy(f).pin_memory() for f in fhs]
+    outs = [torch.empty((1, cfg.N), dtype=ct).pin_memory() for _ in range(K)]
+    plan.transform_host_many(xh, fhh, outs)
+    for k in range(K):
+        assert np.array_equal(outs[k].numpy(), ref[k]), k
+    bad = [x.copy() for x in xs[:3]]
+    bad[2][77, 0] = 0.5                      # outside [-1/2, 1/2): BNFFT_E_NODE_OUT_OF_RANGE
+    with pytest.raises(bn.BnfftError) as ei:
+        plan.transform_host_many([torch.from_numpy(x).pin_memory() for x in bad], fhh[:3], outs[:3])
+    assert ei.value.code == -8 and ei.value.first_bad == 77
+    plan.close()
+
+
 # ----------------------------------------------------------------------------- edge cases
 def test_empty_and_tiny_node_sets(bn, torch):
     plan = bn.Plan(2, 16, 2.0, 3, "sinh", "c128")
