@@ -167,7 +167,8 @@ template <int D>
 __global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(
     const double* __restrict__ x, int64_t n, KeyParams kp, uint32_t* __restrict__ keys,
     unsigned long long* __restrict__ bad, double* __restrict__ xcopy, int aligned16, int bits,
-    uint32_t* __restrict__ hist, SegLayout sl) {
+    uint32_t* __restrict__ hist, SegLayout sl, float4* __restrict__ rec) {
+  // rec (rec3 plans, D = 3): the nodes' 16-B gather records in user order (node_rec3)
   __shared__ uint32_t cnt[1 << kMaxDigitBits];
   const int ndig = 1 << bits;
   const uint32_t mask = ndig - 1;
@@ -223,6 +224,10 @@ __global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(
       if (full) node_key<D>(xv[jj] + D, kp, c1);
       if (c0) atomicMin(bad, ((unsigned long long)i << 4) | (unsigned long long)c0);
       if (c1) atomicMin(bad, ((unsigned long long)(i + 1) << 4) | (unsigned long long)c1);
+    }
+    if (D == 3 && rec) {
+      rec[i] = node_rec3(xv[jj], kp);
+      if (full) rec[i + 1] = node_rec3(xv[jj] + D, kp);
     }
     atomicAdd(&cnt[k0 & mask], 1u);
     if (full) atomicAdd(&cnt[k1 & mask], 1u);
@@ -663,15 +668,16 @@ cudaError_t launch_keys(bnfft_plan_s* p, const double* x, int64_t n) {
   const KeyParams kp = key_params(p);
   cudaError_t e = cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), p->stream);
   if (e != cudaSuccess) return e;
-  if (n > 0 && p->sort_passes > 0 && p->opts.d <= 2) {   // first-pass histogram fused (d <= 2)
+  if (n > 0 && p->sort_passes > 0 && (p->opts.d <= 2 || p->rec3)) {   // first-pass histogram fused
     SegLayout sl;
     sl.ntiles = (n + kSortTile - 1) / kSortTile;
     sl.tpb = std::min<int64_t>(sl.ntiles, (int64_t)1 << std::max(0, p->ub_log2 - kSortTileLog2));
     const int b0 = std::min(p->digit_bits, p->key_bits);
-    auto kfn = p->opts.d == 1 ? keys_hist_kernel<1> : keys_hist_kernel<2>;
+    auto kfn = p->opts.d == 1 ? keys_hist_kernel<1> : p->opts.d == 2 ? keys_hist_kernel<2> : keys_hist_kernel<3>;
     kfn<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(x, n, kp, p->d1_binned ? nullptr : p->d_k0, p->d_bad,
                                                               p->xs_user ? p->d_xs : nullptr,
-                                                              ((uintptr_t)x & 15) == 0 ? 1 : 0, b0, p->d_hist, sl);
+                                                              ((uintptr_t)x & 15) == 0 ? 1 : 0, b0, p->d_hist, sl,
+                                                              p->rec3 ? (float4*)p->d_rec_user : nullptr);
     p->launches++;
   } else if (n > 0) {
     auto kfn = p->opts.d == 1 ? keys_kernel<1> : p->opts.d == 2 ? keys_kernel<2> : keys_kernel<3>;
@@ -750,7 +756,7 @@ cudaError_t launch_sort(bnfft_plan_s* p, const double* x, int64_t n) {
       int shift = pass * bits;
       int b = std::min(bits, p->key_bits - shift);
       int64_t nh = ((int64_t)1 << b) * sl.ntiles;
-      if (pass > 0 || p->opts.d > 2) {   // d <= 2, pass 0: counted by keys_hist_kernel
+      if (pass > 0 || !(p->opts.d <= 2 || p->rec3)) {   // pass 0: counted by keys_hist_kernel
         radix_hist_kernel<<<(unsigned)sl.ntiles, kSortThreads, 0, p->stream>>>(kin, n, shift, b,
                                                                                p->d_hist, sl);
         p->launches++;
