@@ -50,7 +50,7 @@ constexpr int BOXB = (BOX * 8 + 127) / 128 * 128;
 constexpr int REC = 28;                    // words per record (112 B: 16-B slots of 8 consecutive lanes'
                                            // records distinct): wz[8] | wy pairs[8] | wx[8] | meta dst
 constexpr int OFF_REC = NBUF * BOXB;                           // float [NW][32][REC]
-constexpr int SMEM = OFF_REC + NW * 32 * REC * 4;
+constexpr int SMEM = OFF_REC + (NW * 32 + 1) * REC * 4;     // + one pad record (meta prefetch)
 static_assert(OFF_REC % 16 == 0, "16-B aligned records");
 
 }  // namespace g3y
@@ -93,6 +93,10 @@ __device__ __forceinline__ void g3y_produce(const GatherParams<float>& p, const 
     mbar_arrive(bar);
     return;
   }
+#ifdef G3Y_ABL_NOTMA
+  mbar_arrive(bar);
+  return;
+#endif
   const int c0 = Z * 8 - 4;    // z (innermost): even start (16-B aligned rows), one extra element
   const int c1 = Y * 16 - 3;   // y
   const int c2 = X * 8 - 3;    // x
@@ -117,7 +121,11 @@ __device__ __forceinline__ void g3y_fetch(const GatherParams<float>& p, uint32_t
   const uint32_t i = s0 + (uint32_t)lane;
   if (i < e) {
     pj = __ldg(&p.perm[i]);
+#ifdef G3Y_ABL_SEQREC
+    c4 = __ldg(reinterpret_cast<const float4*>(p.xs) + i);
+#else
     c4 = __ldg(reinterpret_cast<const float4*>(p.xs) + pj);
+#endif
   }
 }
 
@@ -169,6 +177,11 @@ __device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32
     const int col = (int)(md >> 3);
     float* r = rec + lane * g3y::REC;
     float w[3][T];
+#ifdef G3Y_ABL_NOTAPS
+    for (int t = 0; t < 3; ++t)
+      for (int q = 0; q < T; ++q) w[t][q] = c4.x * (float)(q + t);
+    if (0)
+#endif
     if (POLY) {
       const float uu[3] = {c4.x, c4.y, c4.z};
       g3y_taps3(p, uu, w);
@@ -215,6 +228,15 @@ template <int OZ>
 __device__ __forceinline__ void g3y_zdot(const float2 (&R0)[16], const float2 (&R1)[16], const float4& wa,
                                          const float4& wb, float2& d0, float2& d1) {
   const float wz[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#ifdef G3Y_ONE_CHAIN
+  d0 = __fmul2_rn(make_float2(wz[0], wz[0]), R0[OZ + 1]);
+  d1 = __fmul2_rn(make_float2(wz[0], wz[0]), R1[OZ + 1]);
+#pragma unroll
+  for (int c = 1; c < 8; ++c) {
+    cmac(d0, wz[c], R0[OZ + 1 + c]);
+    cmac(d1, wz[c], R1[OZ + 1 + c]);
+  }
+#else
   float2 e0 = make_float2(0.f, 0.f), o0 = e0, e1 = e0, o1 = e0;
 #pragma unroll
   for (int c = 0; c < 8; c += 2) {
@@ -225,6 +247,7 @@ __device__ __forceinline__ void g3y_zdot(const float2 (&R0)[16], const float2 (&
   }
   d0 = __fadd2_rn(e0, o0);
   d1 = __fadd2_rn(e1, o1);
+#endif
 }
 
 __device__ __forceinline__ void g3y_wait(uint64_t* bar, uint32_t parity) {
@@ -316,8 +339,15 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
         const int nq = (int)min(32u, ne - s0);
         if (s0 + 32 < ne) g3y_fetch(p, s0 + 32, ne, lane, c4, pj);   // next batch, in flight meanwhile
         float* r = rec;
+        // the next node's meta word is loaded one iteration ahead and the record's weights before
+        // the window advance, shortening the per-node chain of dependent shared-memory loads
+        uint32_t md_n = reinterpret_cast<const uint32_t*>(r)[24];
         for (int q = 0; q < nq; ++q, r += REC) {
-          const uint32_t md = reinterpret_cast<const uint32_t*>(r)[24];
+          const uint32_t md = md_n;
+          const float4 wa = reinterpret_cast<const float4*>(r)[0];
+          const float4 wb = reinterpret_cast<const float4*>(r)[1];
+          const float2 wy = reinterpret_cast<const float2*>(r + 8)[lq];
+          md_n = reinterpret_cast<const uint32_t*>(r + REC)[24];   // (one record past the batch: unused)
           const int col = (int)(md >> 3);
           while (ycur < col) {   // window [ycur, ycur + 8) -> [ycur + 1, ycur + 9): row ycur + 8
             const int rn = ycur + 8;
@@ -327,10 +357,12 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
             }
             ++ycur;
           }
-          const float4 wa = reinterpret_cast<const float4*>(r)[0];
-          const float4 wb = reinterpret_cast<const float4*>(r)[1];
-          const float2 wy = reinterpret_cast<const float2*>(r + 8)[lq];
           float2 d0, d1;
+#ifdef G3Y_ABL_NOZDOT
+          d0 = R0[1 + (md & 1u)];
+          d1 = R1[1 + (md & 1u)];
+          if (0)
+#endif
           switch (md & 7u) {
             case 0: g3y_zdot<0>(R0, R1, wa, wb, d0, d1); break;
             case 1: g3y_zdot<1>(R0, R1, wa, wb, d0, d1); break;
@@ -345,8 +377,10 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
           // the x-plane sums overwrite the node's (consumed) z and y weights
           float2 t = __fmul2_rn(make_float2(wy.x, wy.x), d0);
           cmac(t, wy.y, d1);
+#ifndef G3Y_ABL_NORED
           t = __fadd2_rn(t, make_float2(__shfl_xor_sync(0xffffffffu, t.x, 8), __shfl_xor_sync(0xffffffffu, t.y, 8)));
           t = __fadd2_rn(t, make_float2(__shfl_xor_sync(0xffffffffu, t.x, 16), __shfl_xor_sync(0xffffffffu, t.y, 16)));
+#endif
           if (lq == 0) reinterpret_cast<float2*>(r)[la] = t;
         }
         __syncwarp();
@@ -364,6 +398,9 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
           cmac(f, wx1.w, make_float2(v3.z, v3.w));
           const uint32_t d = reinterpret_cast<const uint32_t*>(rec + lane * REC)[25];
           float2* dp = out + d;
+#ifdef G3Y_ABL_NOSTORE
+          if (f.x == 12345.f)
+#endif
           if (hint_out)
             asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dp), "f"(f.x),
                          "f"(f.y), "l"(pol_out)
