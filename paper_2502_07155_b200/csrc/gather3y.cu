@@ -50,7 +50,7 @@ constexpr int BOXB = (BOX * 8 + 127) / 128 * 128;
 constexpr int REC = 28;                    // words per record (112 B: 16-B slots of 8 consecutive lanes'
                                            // records distinct): wz[8] | wy pairs[8] | wx[8] | meta dst
 constexpr int OFF_REC = NBUF * BOXB;                           // float [NW][32][REC]
-constexpr int SMEM = OFF_REC + (NW * 32 + 1) * REC * 4;     // + one pad record (meta prefetch)
+constexpr int SMEM = OFF_REC + NW * 32 * REC * 4;
 static_assert(OFF_REC % 16 == 0, "16-B aligned records");
 
 }  // namespace g3y
@@ -87,31 +87,17 @@ __device__ __forceinline__ bool g3y_decode(const Geo3y& g, uint32_t v, int& X, i
 // Load item k (virtual index v) into box buffer b, or complete the buffer's phase without data for a
 // hole of the virtual index space (thread of the producing warp only).
 __device__ __forceinline__ void g3y_produce(const GatherParams<float>& p, const CUtensorMap* tm, const Geo3y& g,
-                                            uint32_t v, float2* box, uint64_t* bar, uint64_t pol) {
+                                            uint32_t v, float2* box, uint64_t* bar) {
   int X, Y, Z;
   if (!g3y_decode(g, v, X, Y, Z)) {
     mbar_arrive(bar);
     return;
   }
-#ifdef G3Y_ABL_NOTMA
-  mbar_arrive(bar);
-  return;
-#endif
-  const int c0 = Z * 8 - 4;    // z (innermost): even start (16-B aligned rows), one extra element
-  const int c1 = Y * 16 - 3;   // y
-  const int c2 = X * 8 - 3;    // x
+  const int c[3] = {Z * 8 - 4,    // z (innermost): even start (16-B aligned rows), one extra element
+                    Y * 16 - 3,   // y
+                    X * 8 - 3};   // x
   mbar_expect_tx(bar, (uint32_t)(g3y::BOX * sizeof(float2)));
-  const uint32_t d = smem_u32(box), b = smem_u32(bar);
-  const uint64_t t = reinterpret_cast<uint64_t>(tm);
-  if (p.l2_hint & 2)
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(d), "l"(t), "r"(b), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
-        : "memory");
-  else
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
-        ::"r"(d), "l"(t), "r"(b), "r"(c0), "r"(c1), "r"(c2) : "memory");
+  tma_load_box(tm, box, bar, 3, c);
 }
 
 // Phase B, load part: the permutation entry and the keys kernel's 16-B user-order record (rec3) of
@@ -286,10 +272,6 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
   while ((1 << g.bx) < g.nX) ++g.bx;
   while ((1 << g.byb) < g.nY) ++g.byb;
   while ((1 << g.bzb) < g.nZ) ++g.bzb;
-  uint64_t pol_out = 0, pol_box = 0;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_out));
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_box));
-  const bool hint_out = (p.l2_hint & 1) != 0;
 
   if (tid == 0) {
     for (int b = 0; b < NBUF; ++b) {
@@ -300,32 +282,42 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
     for (int b = 0; b < NBUF; ++b) {
       s_tag[b] = b;
       const uint32_t v = blockIdx.x + (uint32_t)b * G;
-      if (v < nvirt) g3y_produce(p, tmap, g, v, boxes + (size_t)b * (BOXB / 8), &full[b], pol_box);
+      if (v < nvirt) g3y_produce(p, tmap, g, v, boxes + (size_t)b * (BOXB / 8), &full[b]);
     }
   }
   __syncthreads();
 
+  // the warp's x-line node range of item k (key offsets; empty for holes and x-lines past L)
+  auto xline_range = [&](uint32_t k, uint32_t& b0, uint32_t& e0) {
+    b0 = e0 = 0;
+    const uint32_t v = blockIdx.x + k * G;
+    if (v >= nvirt) return;
+    int X, Y, Z;
+    if (!g3y_decode(g, v, X, Y, Z)) return;
+    const int cx = X * 8 + wt;
+    if (cx >= (int)p.L) return;
+    const int64_t key = ((int64_t)cx * p.nb[1] + Y) * p.nb[2] + Z;
+    b0 = __ldg(&p.key_start[key]);
+    e0 = __ldg(&p.key_start[key + 1]);
+  };
+  // The first batch of an item's nodes (permutation entries and records) is fetched during the
+  // previous item's last batch, and the next item's key offsets at the start of the current one, so
+  // no global-memory latency is exposed at item boundaries.
+  uint32_t nb0, ne;
+  xline_range((uint32_t)team, nb0, ne);
+  float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t pj = 0;
+  if (nb0 < ne) g3y_fetch(p, nb0, ne, lane, c4, pj);
   for (uint32_t k = (uint32_t)team;; k += 2) {
     const uint32_t v = blockIdx.x + k * G;
     if (v >= nvirt) break;
     const int b = (int)(k % NBUF);
-    int X, Y, Z;
-    const bool real = g3y_decode(g, v, X, Y, Z);
-    uint32_t nb0 = 0, ne = 0;
-    const int cx = X * 8 + wt;
-    if (real && cx < (int)p.L) {
-      const int64_t key = ((int64_t)cx * p.nb[1] + Y) * p.nb[2] + Z;
-      nb0 = __ldg(&p.key_start[key]);
-      ne = __ldg(&p.key_start[key + 1]);
-    }
+    uint32_t nb0_n, ne_n;
+    xline_range(k + 2, nb0_n, ne_n);   // in flight during this item
     const float2* box = boxes + (size_t)b * (BOXB / 8);
     const int xa = wt + la;          // box x index of the lane's rows
-    float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t pj = 0;
-    if (nb0 < ne) {   // overlaps the box's TMA
-      g3y_fetch(p, nb0, ne, lane, c4, pj);
-      g3y_phase_b<POLY>(p, nb0, ne, rec, lane, c4, pj);
-    }
+    if (nb0 < ne) g3y_phase_b<POLY>(p, nb0, ne, rec, lane, c4, pj);   // overlaps the box's TMA
+    else if (nb0_n < ne_n) g3y_fetch(p, nb0_n, ne_n, lane, c4, pj);
     while (s_tag[b] != (int)k) {
     }
     g3y_wait(&full[b], (k / NBUF) & 1u);
@@ -338,17 +330,11 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
       for (uint32_t s0 = nb0;;) {
         const int nq = (int)min(32u, ne - s0);
         if (s0 + 32 < ne) g3y_fetch(p, s0 + 32, ne, lane, c4, pj);   // next batch, in flight meanwhile
-        float* r = rec;
-        // the next node's meta word is loaded one iteration ahead and the record's weights before
-        // the window advance, shortening the per-node chain of dependent shared-memory loads
-        uint32_t md_n = reinterpret_cast<const uint32_t*>(r)[24];
-        for (int q = 0; q < nq; ++q, r += REC) {
-          const uint32_t md = md_n;
-          const float4 wa = reinterpret_cast<const float4*>(r)[0];
-          const float4 wb = reinterpret_cast<const float4*>(r)[1];
-          const float2 wy = reinterpret_cast<const float2*>(r + 8)[lq];
-          md_n = reinterpret_cast<const uint32_t*>(r + REC)[24];   // (one record past the batch: unused)
-          const int col = (int)(md >> 3);
+        else if (nb0_n < ne_n) g3y_fetch(p, nb0_n, ne_n, lane, c4, pj);   // the next item's first batch
+        // Nodes are processed in pairs whose instruction streams interleave: node B's record loads,
+        // window advance and z-dots issue while node A's shuffle sum is in flight (the per-node chain
+        // of dependent shared-memory loads, branches and shuffles is the kernel's critical path).
+        auto advance = [&](int col) {
           while (ycur < col) {   // window [ycur, ycur + 8) -> [ycur + 1, ycur + 9): row ycur + 8
             const int rn = ycur + 8;
             if (lq == (rn & 3)) {
@@ -357,13 +343,9 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
             }
             ++ycur;
           }
-          float2 d0, d1;
-#ifdef G3Y_ABL_NOZDOT
-          d0 = R0[1 + (md & 1u)];
-          d1 = R1[1 + (md & 1u)];
-          if (0)
-#endif
-          switch (md & 7u) {
+        };
+        auto zdot = [&](uint32_t oz, const float4& wa, const float4& wb, float2& d0, float2& d1) {
+          switch (oz) {
             case 0: g3y_zdot<0>(R0, R1, wa, wb, d0, d1); break;
             case 1: g3y_zdot<1>(R0, R1, wa, wb, d0, d1); break;
             case 2: g3y_zdot<2>(R0, R1, wa, wb, d0, d1); break;
@@ -373,14 +355,58 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
             case 6: g3y_zdot<6>(R0, R1, wa, wb, d0, d1); break;
             default: g3y_zdot<7>(R0, R1, wa, wb, d0, d1); break;
           }
-          // y contraction of the lane's two rows, then the sum over the 4 row lanes of x-plane a;
-          // the x-plane sums overwrite the node's (consumed) z and y weights
+        };
+        // y contraction of the lane's two rows (then summed over the 4 row lanes of x-plane a; the
+        // x-plane sums overwrite the node's consumed z and y weights)
+        auto ycon = [&](const float2& wy, const float2& d0, const float2& d1) {
           float2 t = __fmul2_rn(make_float2(wy.x, wy.x), d0);
           cmac(t, wy.y, d1);
-#ifndef G3Y_ABL_NORED
-          t = __fadd2_rn(t, make_float2(__shfl_xor_sync(0xffffffffu, t.x, 8), __shfl_xor_sync(0xffffffffu, t.y, 8)));
-          t = __fadd2_rn(t, make_float2(__shfl_xor_sync(0xffffffffu, t.x, 16), __shfl_xor_sync(0xffffffffu, t.y, 16)));
-#endif
+          return t;
+        };
+        auto shfl2 = [&](const float2& t, int o) {
+          return make_float2(__shfl_xor_sync(0xffffffffu, t.x, o), __shfl_xor_sync(0xffffffffu, t.y, o));
+        };
+        float* r = rec;
+        int q = 0;
+        for (; q + 1 < nq; q += 2, r += 2 * REC) {
+          float* rB = r + REC;
+          const uint32_t mdA = reinterpret_cast<const uint32_t*>(r)[24];
+          const uint32_t mdB = reinterpret_cast<const uint32_t*>(rB)[24];
+          const float4 waA = reinterpret_cast<const float4*>(r)[0];
+          const float4 wbA = reinterpret_cast<const float4*>(r)[1];
+          const float2 wyA = reinterpret_cast<const float2*>(r + 8)[lq];
+          advance((int)(mdA >> 3));
+          float2 d0, d1;
+          zdot(mdA & 7u, waA, wbA, d0, d1);
+          float2 tA = ycon(wyA, d0, d1);
+          const float2 sA = shfl2(tA, 8);
+          const float4 waB = reinterpret_cast<const float4*>(rB)[0];
+          const float4 wbB = reinterpret_cast<const float4*>(rB)[1];
+          const float2 wyB = reinterpret_cast<const float2*>(rB + 8)[lq];
+          advance((int)(mdB >> 3));
+          zdot(mdB & 7u, waB, wbB, d0, d1);
+          float2 tB = ycon(wyB, d0, d1);
+          const float2 sB = shfl2(tB, 8);
+          tA = __fadd2_rn(tA, sA);
+          tB = __fadd2_rn(tB, sB);
+          tA = __fadd2_rn(tA, shfl2(tA, 16));
+          tB = __fadd2_rn(tB, shfl2(tB, 16));
+          if (lq == 0) {
+            reinterpret_cast<float2*>(r)[la] = tA;
+            reinterpret_cast<float2*>(rB)[la] = tB;
+          }
+        }
+        if (q < nq) {   // odd node
+          const uint32_t md = reinterpret_cast<const uint32_t*>(r)[24];
+          const float4 wa = reinterpret_cast<const float4*>(r)[0];
+          const float4 wb = reinterpret_cast<const float4*>(r)[1];
+          const float2 wy = reinterpret_cast<const float2*>(r + 8)[lq];
+          advance((int)(md >> 3));
+          float2 d0, d1;
+          zdot(md & 7u, wa, wb, d0, d1);
+          float2 t = ycon(wy, d0, d1);
+          t = __fadd2_rn(t, shfl2(t, 8));
+          t = __fadd2_rn(t, shfl2(t, 16));
           if (lq == 0) reinterpret_cast<float2*>(r)[la] = t;
         }
         __syncwarp();
@@ -397,16 +423,7 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
           cmac(f, wx1.z, make_float2(v3.x, v3.y));
           cmac(f, wx1.w, make_float2(v3.z, v3.w));
           const uint32_t d = reinterpret_cast<const uint32_t*>(rec + lane * REC)[25];
-          float2* dp = out + d;
-#ifdef G3Y_ABL_NOSTORE
-          if (f.x == 12345.f)
-#endif
-          if (hint_out)
-            asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dp), "f"(f.x),
-                         "f"(f.y), "l"(pol_out)
-                         : "memory");
-          else
-            *dp = f;
+          out[d] = f;
         }
         __syncwarp();   // records free for the next batch
         s0 += 32;
@@ -426,9 +443,11 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         s_tag[b] = (int)kn;
         __threadfence_block();
-        if (vn < nvirt) g3y_produce(p, tmap, g, vn, boxes + (size_t)b * (BOXB / 8), &full[b], pol_box);
+        if (vn < nvirt) g3y_produce(p, tmap, g, vn, boxes + (size_t)b * (BOXB / 8), &full[b]);
       }
     }
+    nb0 = nb0_n;
+    ne = ne_n;
   }
 }
 
