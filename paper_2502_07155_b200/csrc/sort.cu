@@ -517,23 +517,46 @@ __global__ void __launch_bounds__(kSortThreads, SCATTER_MIN_CTAS) radix_scatter_
   }
 }
 
-// K3: sorted node copy xs[i] = x[perm[i]] and offsets over the full sort key (user block, bin):
-// key'(i) = (i >> ub_log2) * nbins + skey[i] (sorted position i lies in user block i >> ub_log2).
+// K3: key offsets over the full sort key (user block, bin): key'(i) = (i >> ub_log2) * nbins +
+// (skey[i] >> colbits) (sorted position i lies in user block i >> ub_log2); key_start[b] = first sorted
+// position with key' >= b.  Four sorted keys per thread (16-byte loads) plus the preceding one.
+__device__ __forceinline__ int64_t full_key(const uint32_t* skeys, int64_t i, int ub_log2, int64_t nbins,
+                                            int colbits, uint32_t sk) {
+  (void)skeys;
+  return (i >> ub_log2) * nbins + (int64_t)(sk >> colbits);
+}
+
 __global__ void build_kernel(const double* __restrict__ x, const uint32_t* __restrict__ perm,
                              const uint32_t* __restrict__ skeys, double* __restrict__ xs,
                              uint32_t* __restrict__ key_start, int64_t n, int d, int64_t nbins,
                              int ub_log2, int64_t nkeys, int colbits) {
-  // colbits: the sorted keys carry a minor digit below the bin (rec3); offsets are per bin
-  // xs == nullptr: offsets only (plans that keep the nodes in user order)
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < n && xs) {
-      uint32_t j = perm[i];
-      for (int t = 0; t < d; ++t) xs[i * d + t] = x[(int64_t)j * d + t];
+  (void)x;
+  (void)perm;
+  (void)xs;
+  (void)d;
+  const int64_t nq = (n + 4) / 4;   // groups of 4 positions covering [0, n]
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nq; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = 4 * g;
+    uint32_t k4[4];
+    if (i0 + 4 <= n && (((uintptr_t)(skeys + i0)) & 15) == 0) {
+      const uint4 q = *reinterpret_cast<const uint4*>(skeys + i0);
+      k4[0] = q.x;
+      k4[1] = q.y;
+      k4[2] = q.z;
+      k4[3] = q.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) k4[j] = i0 + j < n ? skeys[i0 + j] : 0u;
     }
-    int64_t kprev = (i == 0) ? -1 : (((i - 1) >> ub_log2) * nbins + (int64_t)(skeys[i - 1] >> colbits));
-    int64_t kcur = (i == n) ? nkeys : ((i >> ub_log2) * nbins + (int64_t)(skeys[i] >> colbits));
-    for (int64_t b = kprev + 1; b <= kcur; ++b) key_start[b] = (uint32_t)i;
+    int64_t kprev = i0 == 0 ? -1 : full_key(skeys, i0 - 1, ub_log2, nbins, colbits, skeys[i0 - 1]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t i = i0 + j;
+      if (i > n) break;
+      const int64_t kcur = i == n ? nkeys : full_key(skeys, i, ub_log2, nbins, colbits, k4[j]);
+      for (int64_t b = kprev + 1; b <= kcur; ++b) key_start[b] = (uint32_t)i;
+      kprev = kcur;
+    }
   }
 }
 
@@ -820,7 +843,7 @@ cudaError_t launch_build(bnfft_plan_s* p, const double* x, int64_t n) {
     p->launches++;
     return cudaGetLastError();
   }
-  build_kernel<<<grid_for(n + 1, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys,
+  build_kernel<<<grid_for((n + 4) / 4, 256), 256, 0, p->stream>>>(x, p->d_perm, p->d_skeys,
                                                             nullptr,   // xs comes from the sort
                                                             p->d_bin_start, n, p->opts.d,
                                                             p->nbins, p->ub_log2, p->nkeys, p->col_bits);
