@@ -2,6 +2,7 @@
 #include <cuda.h>
 
 #include <cstring>
+#include <vector>
 
 #include "gather_impl.cuh"
 
@@ -17,6 +18,7 @@ const void* gather3y_kernel_ptr(bool poly);
 size_t gather3y_smem();
 int gather3y_threads();
 void gather3y_box(int* ext);
+void gather3y_item_table(int64_t nX, int64_t nY, int64_t nZ, std::vector<uint32_t>& tab);
 
 // d = 3, m = 4, complex64, batch 1: a specialised kernel chosen at plan creation (p->g3_kind) -- the
 // y-sweep kernel gather3y (gather3y.cu, x-line bins of 1 x 16 x 8 cells) by default; the half-warp
@@ -152,12 +154,21 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  // y-sweep plans: the decoded item table (gather3y_item_table) follows the tensor map in the same
+  // allocation (the kernel reads it at tmap + 1)
+  std::vector<uint32_t> items;
+  if (use_ysweep3(p)) gather3y_item_table((p->L + 7) >> 3, p->nb_dim[1], p->nb_dim[2], items);
   if (!p->d_tmap) {
-    e = cudaMalloc((void**)&p->d_tmap, sizeof(CUtensorMap));
+    e = cudaMalloc((void**)&p->d_tmap, sizeof(CUtensorMap) + items.size() * sizeof(uint32_t));
     if (e != cudaSuccess) return e;
   }
   e = cudaMemcpyAsync(p->d_tmap, &p->tmap, sizeof(CUtensorMap), cudaMemcpyHostToDevice, p->stream);
   if (e != cudaSuccess) return e;
+  if (!items.empty()) {
+    e = cudaMemcpyAsync(p->d_tmap + 1, items.data(), items.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                        p->stream);
+    if (e != cudaSuccess) return e;
+  }
   return cudaStreamSynchronize(p->stream);
 }
 constexpr int kMaxSegPerRound = 32;

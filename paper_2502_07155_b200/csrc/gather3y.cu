@@ -35,6 +35,8 @@
 // permutation of the node set.
 #include <cuda.h>
 
+#include <vector>
+
 #include "gather_impl.cuh"
 
 namespace bnfft {
@@ -66,33 +68,37 @@ void gather3y_box(int* ext) {
 // Items: groups of 8 x-lines (X, by, bz), visited in a Morton order with unequal bit counts per
 // dimension (dense for power-of-two grids: every virtual index is a real item).  Item k of a CTA is
 // the virtual index blockIdx.x + k * gridDim.x, so consecutive CTAs work on neighbouring items and
-// their boxes' halos are served from L2.
-struct Geo3y {
-  int bx, byb, bzb;   // bits per dimension (X, by, bz)
-  int nX, nY, nZ;     // items per dimension
-};
+// their boxes' halos are served from L2.  The decoded items come from a plan-time table (one word per
+// virtual index: X | Y << 10 | Z << 20, kG3yHole for holes), written by gather3y_item_table.
+constexpr uint32_t kG3yHole = 0xffffffffu;
 
-__device__ __forceinline__ bool g3y_decode(const Geo3y& g, uint32_t v, int& X, int& Y, int& Z) {
-  X = Y = Z = 0;
-  int bit = 0;
-#pragma unroll
-  for (int l = 0; l < 10; ++l) {
-    if (l < g.bzb) { Z |= (int)((v >> bit) & 1u) << l; ++bit; }
-    if (l < g.byb) { Y |= (int)((v >> bit) & 1u) << l; ++bit; }
-    if (l < g.bx) { X |= (int)((v >> bit) & 1u) << l; ++bit; }
+void gather3y_item_table(int64_t nX, int64_t nY, int64_t nZ, std::vector<uint32_t>& tab) {
+  int bx = 0, byb = 0, bzb = 0;
+  while (((int64_t)1 << bx) < nX) ++bx;
+  while (((int64_t)1 << byb) < nY) ++byb;
+  while (((int64_t)1 << bzb) < nZ) ++bzb;
+  const int64_t nvirt = (int64_t)1 << (bx + byb + bzb);
+  tab.assign((size_t)nvirt, kG3yHole);
+  for (int64_t v = 0; v < nvirt; ++v) {
+    int64_t X = 0, Y = 0, Z = 0;
+    int bit = 0;
+    for (int l = 0; l < 30; ++l) {
+      if (l < bzb) { Z |= ((v >> bit) & 1) << l; ++bit; }
+      if (l < byb) { Y |= ((v >> bit) & 1) << l; ++bit; }
+      if (l < bx) { X |= ((v >> bit) & 1) << l; ++bit; }
+    }
+    if (X < nX && Y < nY && Z < nZ) tab[(size_t)v] = (uint32_t)(X | (Y << 10) | (Z << 20));
   }
-  return X < g.nX && Y < g.nY && Z < g.nZ;
 }
 
-// Load item k (virtual index v) into box buffer b, or complete the buffer's phase without data for a
-// hole of the virtual index space (thread of the producing warp only).
-__device__ __forceinline__ void g3y_produce(const GatherParams<float>& p, const CUtensorMap* tm, const Geo3y& g,
-                                            uint32_t v, float2* box, uint64_t* bar) {
-  int X, Y, Z;
-  if (!g3y_decode(g, v, X, Y, Z)) {
+// Load the item `it` (table word) into box buffer b, or complete the buffer's phase without data for
+// a hole of the virtual index space (one thread).
+__device__ __forceinline__ void g3y_produce(const CUtensorMap* tm, uint32_t it, float2* box, uint64_t* bar) {
+  if (it == kG3yHole) {
     mbar_arrive(bar);
     return;
   }
+  const int X = (int)(it & 1023u), Y = (int)((it >> 10) & 1023u), Z = (int)(it >> 20);
   const int c[3] = {Z * 8 - 4,    // z (innermost): even start (16-B aligned rows), one extra element
                     Y * 16 - 3,   // y
                     X * 8 - 3};   // x
@@ -115,9 +121,9 @@ __device__ __forceinline__ void g3y_fetch(const GatherParams<float>& p, uint32_t
   }
 }
 
-// The 24 taps of a node (tap polynomials, R1; the same operations and order as all_taps): the three
-// dimensions' Horner chains run interleaved and share the coefficient operands; Kronecker nodes
-// (u == 0 or 1 in a dimension) take the exact 0/1 taps (interpolation property).
+// The 8 taps of a node in one dimension (tap polynomials, R1; the same operations and order as
+// all_taps): the Horner chains of the even/odd parts run on FFMA2 and share the coefficient operands.
+// Kronecker nodes (u == 0 or 1) are fixed up by g3y_kron (exact 0/1 taps).
 __device__ __forceinline__ void g3y_taps1(const GatherParams<float>& p, const float u, float (&w)[8]) {
   constexpr int m = 4, NH = PolyH<float>::NH;
   const float x = fmaf(2.0f, u, -1.0f);
@@ -136,46 +142,53 @@ __device__ __forceinline__ void g3y_taps1(const GatherParams<float>& p, const fl
     w[0] *= sqrt_r((1.0f - u) * ((float)(2 * m - 1) + u)) * p.inv_m;
     w[2 * m - 1] *= sqrt_r(u * ((float)(2 * m) - u)) * p.inv_m;
   }
-  // Kronecker node (interpolation property): exact 0/1 taps, by selects
+}
+
+// Kronecker node (interpolation property): exact 0/1 taps, by selects
+__device__ __forceinline__ void g3y_kron(const float u, float (&w)[8]) {
+  constexpr int m = 4;
   const bool h0 = u == 0.0f, h1 = u == 1.0f;
 #pragma unroll
   for (int i = 0; i < 2 * m; ++i) w[i] = (h0 | h1) ? ((h0 ? i == m - 1 : i == m) ? 1.0f : 0.0f) : w[i];
 }
 
-// The 24 taps of a node from the tap polynomials (R1): the same operations and order as all_taps,
-// without its generic per-tap fallback branch.
-__device__ __forceinline__ void g3y_taps3(const GatherParams<float>& p, const float (&u)[3], float (&w)[3][8]) {
-#pragma unroll
-  for (int t = 0; t < 3; ++t) g3y_taps1(p, u[t], w[t]);
-}
-
 // Phase B: records of sorted nodes [s0, min(s0 + 32, e)) (lane k: node s0 + k; the sort key's minor
 // digit puts an x-line's nodes in y-column order): the 24 tap weights (tap polynomials, R1), the y
 // weights as the pairs each row-lane group needs at the node's column, (column, z offset) and the
-// destination.
+// destination.  All lanes evaluate taps (idle lanes on u = 1/2) so that the rare Kronecker fix-up is a
+// warp vote.
 template <bool POLY>
 __device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32_t s0, uint32_t e, float* rec,
                                             int lane, const float4 c4, const uint32_t pj) {
   constexpr int T = g3y::T;
   const uint32_t i = s0 + (uint32_t)lane;
-  if (i < e) {
+  const bool act = i < e;
+  float w[3][T];
+  if (POLY) {
+    const float uu[3] = {act ? c4.x : 0.5f, act ? c4.y : 0.5f, act ? c4.z : 0.5f};
+#ifdef G3Y_ABL_NOTAPS
+    for (int t = 0; t < 3; ++t)
+      for (int q = 0; q < T; ++q) w[t][q] = uu[0] * (float)(q + t);
+#else
+#pragma unroll
+    for (int t = 0; t < 3; ++t) g3y_taps1(p, uu[t], w[t]);
+    bool kr = false;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) kr |= (uu[t] == 0.0f) | (uu[t] == 1.0f);
+    if (__any_sync(0xffffffffu, kr)) {
+#pragma unroll
+      for (int t = 0; t < 3; ++t) g3y_kron(uu[t], w[t]);
+    }
+#endif
+  } else if (act) {
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.x, p), p, w[0]);
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.y, p), p, w[1]);
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.z, p), p, w[2]);
+  }
+  if (act) {
     const uint32_t md = __float_as_uint(c4.w);
     const int col = (int)(md >> 3);
     float* r = rec + lane * g3y::REC;
-    float w[3][T];
-#ifdef G3Y_ABL_NOTAPS
-    for (int t = 0; t < 3; ++t)
-      for (int q = 0; q < T; ++q) w[t][q] = c4.x * (float)(q + t);
-    if (0)
-#endif
-    if (POLY) {
-      const float uu[3] = {c4.x, c4.y, c4.z};
-      g3y_taps3(p, uu, w);
-    } else {
-      all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.x, p), p, w[0]);
-      all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.y, p), p, w[1]);
-      all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.z, p), p, w[2]);
-    }
     reinterpret_cast<float4*>(r)[2] = make_float4(w[1][0], w[1][1], w[1][2], w[1][3]);
     reinterpret_cast<float4*>(r)[3] = make_float4(w[1][4], w[1][5], w[1][6], w[1][7]);
     // row-lane group q holds window rows b = (q - col) & 7 and b ^ 4: pairs (wy[b], wy[b ^ 4])
@@ -248,6 +261,12 @@ __device__ __forceinline__ void g3y_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Work distribution: slots s = 0, 1, 2, ... of a CTA are the x-lines (item s >> 3, x-line s & 7),
+// claimed in order by whichever warp is free (shared-memory counter), so a slow x-line does not hold
+// up the other warps of its item; a warp claims its next slot while it works on the current one and
+// prefetches that slot's key offsets and first record batch.  Item k's box lives in ring buffer k % 3:
+// the warp completing the item's eighth x-line loads item k + 3 into it.  (No deadlock: the oldest
+// unfinished item's box is always loaded, and every warp holding one of its slots works on it.)
 template <bool POLY>
 __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_constant__ GatherParams<float> p,
                                                               const CUtensorMap* __restrict__ tmap) {
@@ -256,24 +275,18 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
   __shared__ __align__(8) uint64_t full[NBUF];
   __shared__ int s_done[NBUF];
   __shared__ volatile int s_tag[NBUF];   // item whose box buffer b holds or is loading
+  __shared__ uint32_t s_next;             // slot counter
   float2* const boxes = reinterpret_cast<float2*>(g3y_smem);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int team = wid >> 3, wt = wid & 7;
   const int la = lane & 7, lq = lane >> 3;
   float* const rec = reinterpret_cast<float*>(g3y_smem + OFF_REC) + wid * 32 * REC;
   float2* __restrict__ out = (float2*)p.out;
   const uint32_t G = gridDim.x;
   const uint32_t nvirt = (uint32_t)p.nkeys_morton;
-  Geo3y g;
-  g.nX = (int)((p.L + 7) >> 3);
-  g.nY = (int)p.nb[1];
-  g.nZ = (int)p.nb[2];
-  g.bx = g.byb = g.bzb = 0;
-  while ((1 << g.bx) < g.nX) ++g.bx;
-  while ((1 << g.byb) < g.nY) ++g.byb;
-  while ((1 << g.bzb) < g.nZ) ++g.bzb;
+  const uint32_t* __restrict__ items = reinterpret_cast<const uint32_t*>(tmap + 1);   // gather3y_item_table
 
   if (tid == 0) {
+    s_next = 0;
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&full[b], 1);
       s_done[b] = 0;
@@ -282,42 +295,55 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
     for (int b = 0; b < NBUF; ++b) {
       s_tag[b] = b;
       const uint32_t v = blockIdx.x + (uint32_t)b * G;
-      if (v < nvirt) g3y_produce(p, tmap, g, v, boxes + (size_t)b * (BOXB / 8), &full[b]);
+      if (v < nvirt) g3y_produce(tmap, __ldg(&items[v]), boxes + (size_t)b * (BOXB / 8), &full[b]);
     }
   }
   __syncthreads();
 
-  // the warp's x-line node range of item k (key offsets; empty for holes and x-lines past L)
-  auto xline_range = [&](uint32_t k, uint32_t& b0, uint32_t& e0) {
-    b0 = e0 = 0;
-    const uint32_t v = blockIdx.x + k * G;
-    if (v >= nvirt) return;
-    int X, Y, Z;
-    if (!g3y_decode(g, v, X, Y, Z)) return;
-    const int cx = X * 8 + wt;
-    if (cx >= (int)p.L) return;
-    const int64_t key = ((int64_t)cx * p.nb[1] + Y) * p.nb[2] + Z;
-    b0 = __ldg(&p.key_start[key]);
-    e0 = __ldg(&p.key_start[key + 1]);
+  // claim the next slot; its item k (or ~0u past the CTA's last item), x-line w and node range
+  struct Slot {
+    uint32_t k, b0, e0;
+    int w;
   };
-  // The first batch of an item's nodes (permutation entries and records) is fetched during the
-  // previous item's last batch, and the next item's key offsets at the start of the current one, so
-  // no global-memory latency is exposed at item boundaries.
-  uint32_t nb0, ne;
-  xline_range((uint32_t)team, nb0, ne);
+  auto claim = [&]() {
+    Slot s;
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(&s_next, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    s.k = c >> 3;
+    s.w = (int)(c & 7u);
+    s.b0 = s.e0 = 0;
+    const uint32_t v = blockIdx.x + s.k * G;
+    if (v >= nvirt) {
+      s.k = ~0u;
+      return s;
+    }
+    const uint32_t it = __ldg(&items[v]);
+    if (it == kG3yHole) return s;
+    const int X = (int)(it & 1023u), Y = (int)((it >> 10) & 1023u), Z = (int)(it >> 20);
+    const int cx = X * 8 + s.w;
+    if (cx >= (int)p.L) return s;
+    const int64_t key = ((int64_t)cx * p.nb[1] + Y) * p.nb[2] + Z;
+    s.b0 = __ldg(&p.key_start[key]);
+    s.e0 = __ldg(&p.key_start[key + 1]);
+    return s;
+  };
+  // The first batch of a slot's nodes (permutation entries and records) is fetched during the
+  // previous slot's last batch, and the next slot's key offsets at the start of the current one, so
+  // no global-memory latency is exposed at slot boundaries.
+  Slot cur = claim();
+  Slot nxt = claim();
   float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t pj = 0;
-  if (nb0 < ne) g3y_fetch(p, nb0, ne, lane, c4, pj);
-  for (uint32_t k = (uint32_t)team;; k += 2) {
-    const uint32_t v = blockIdx.x + k * G;
-    if (v >= nvirt) break;
+  if (cur.b0 < cur.e0) g3y_fetch(p, cur.b0, cur.e0, lane, c4, pj);
+  while (cur.k != ~0u) {
+    const uint32_t k = cur.k;
     const int b = (int)(k % NBUF);
-    uint32_t nb0_n, ne_n;
-    xline_range(k + 2, nb0_n, ne_n);   // in flight during this item
+    const uint32_t nb0 = cur.b0, ne = cur.e0;
     const float2* box = boxes + (size_t)b * (BOXB / 8);
-    const int xa = wt + la;          // box x index of the lane's rows
+    const int xa = cur.w + la;       // box x index of the lane's rows
     if (nb0 < ne) g3y_phase_b<POLY>(p, nb0, ne, rec, lane, c4, pj);   // overlaps the box's TMA
-    else if (nb0_n < ne_n) g3y_fetch(p, nb0_n, ne_n, lane, c4, pj);
+    else if (nxt.b0 < nxt.e0) g3y_fetch(p, nxt.b0, nxt.e0, lane, c4, pj);
     while (s_tag[b] != (int)k) {
     }
     g3y_wait(&full[b], (k / NBUF) & 1u);
@@ -330,7 +356,7 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
       for (uint32_t s0 = nb0;;) {
         const int nq = (int)min(32u, ne - s0);
         if (s0 + 32 < ne) g3y_fetch(p, s0 + 32, ne, lane, c4, pj);   // next batch, in flight meanwhile
-        else if (nb0_n < ne_n) g3y_fetch(p, nb0_n, ne_n, lane, c4, pj);   // the next item's first batch
+        else if (nxt.b0 < nxt.e0) g3y_fetch(p, nxt.b0, nxt.e0, lane, c4, pj);   // the next slot's first batch
         // Nodes are processed in pairs whose instruction streams interleave: node B's record loads,
         // window advance and z-dots issue while node A's shuffle sum is in flight (the per-node chain
         // of dependent shared-memory loads, branches and shuffles is the kernel's critical path).
@@ -366,6 +392,7 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
         auto shfl2 = [&](const float2& t, int o) {
           return make_float2(__shfl_xor_sync(0xffffffffu, t.x, o), __shfl_xor_sync(0xffffffffu, t.y, o));
         };
+        const bool odd_q = (lq & 1) != 0;
         float* r = rec;
         int q = 0;
         for (; q + 1 < nq; q += 2, r += 2 * REC) {
@@ -378,23 +405,21 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
           advance((int)(mdA >> 3));
           float2 d0, d1;
           zdot(mdA & 7u, waA, wbA, d0, d1);
-          float2 tA = ycon(wyA, d0, d1);
-          const float2 sA = shfl2(tA, 8);
+          const float2 tA = ycon(wyA, d0, d1);
           const float4 waB = reinterpret_cast<const float4*>(rB)[0];
           const float4 wbB = reinterpret_cast<const float4*>(rB)[1];
           const float2 wyB = reinterpret_cast<const float2*>(rB + 8)[lq];
           advance((int)(mdB >> 3));
           zdot(mdB & 7u, waB, wbB, d0, d1);
-          float2 tB = ycon(wyB, d0, d1);
-          const float2 sB = shfl2(tB, 8);
-          tA = __fadd2_rn(tA, sA);
-          tB = __fadd2_rn(tB, sB);
-          tA = __fadd2_rn(tA, shfl2(tA, 16));
-          tB = __fadd2_rn(tB, shfl2(tB, 16));
-          if (lq == 0) {
-            reinterpret_cast<float2*>(r)[la] = tA;
-            reinterpret_cast<float2*>(rB)[la] = tB;
-          }
+          const float2 tB = ycon(wyB, d0, d1);
+          // transposed sum over the 4 row lanes: lanes with even q keep node A, odd q node B, and
+          // receive their partner's share of it (the same additions, in the same order, as a
+          // butterfly per node: (q0 + q1) + (q2 + q3))
+          float2 kp = odd_q ? tB : tA;
+          const float2 sd = odd_q ? tA : tB;
+          kp = __fadd2_rn(kp, shfl2(sd, 8));
+          kp = __fadd2_rn(kp, shfl2(kp, 16));
+          if (lq < 2) reinterpret_cast<float2*>(lq ? rB : r)[la] = kp;
         }
         if (q < nq) {   // odd node
           const uint32_t md = reinterpret_cast<const uint32_t*>(r)[24];
@@ -431,7 +456,7 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
         g3y_phase_b<POLY>(p, s0, ne, rec, lane, c4, pj);
       }
     }
-    // ---- release box buffer b; the team's last warp loads item k + NBUF into it
+    // ---- release box buffer b; the warp completing the item's eighth x-line loads item k + NBUF
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -443,11 +468,11 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         s_tag[b] = (int)kn;
         __threadfence_block();
-        if (vn < nvirt) g3y_produce(p, tmap, g, vn, boxes + (size_t)b * (BOXB / 8), &full[b]);
+        if (vn < nvirt) g3y_produce(tmap, __ldg(&items[vn]), boxes + (size_t)b * (BOXB / 8), &full[b]);
       }
     }
-    nb0 = nb0_n;
-    ne = ne_n;
+    cur = nxt;
+    if (cur.k != ~0u) nxt = claim();
   }
 }
 

@@ -377,6 +377,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   // 8 x 8 x 16 cells (innermost box extent 16 + 2m = 24: conflict-free shared-memory rows).
   const bool coop3 = o->d == 3 && o->m == 4 && o->prec == BNFFT_C64 && o->batch == 1 && lgL >= 4;
   p->g3_kind = getenv("BNFFT_GATHER3S") ? 2 : getenv("BNFFT_GATHER3C") ? 1 : 0;
+  if (p->g3_kind == 0 && L > 8192) p->g3_kind = 1;   // y-sweep item table: 10-bit item coordinates
   p->rec3 = coop3 && p->g3_kind == 0;
   for (int t = 0; t < 3; ++t) {
     int lt = lg;
