@@ -49,11 +49,14 @@ constexpr int BX = 15, BY = 23, BZ = 18;   // box extents: 8 + 7, 16 + 7, 8 + 8 
                                            // 23*18*8 B = 112 mod 128 -> conflict-free row loads)
 constexpr int BOX = BX * BY * BZ;          // complex64 elements
 constexpr int BOXB = (BOX * 8 + 127) / 128 * 128;
-constexpr int REC = 28;                    // words per record (112 B: 16-B slots of 8 consecutive lanes'
-                                           // records distinct): wz[8] | wy pairs[8] | wx[8] | meta dst
+constexpr int REC = 24;                    // words per record: wz[8] | wy pairs[8] | wx[8]
+constexpr int GN = 8;                      // nodes per reduction group
 constexpr int OFF_REC = NBUF * BOXB;                           // float [NW][32][REC]
-constexpr int SMEM = OFF_REC + NW * 32 * REC * 4;
-static_assert(OFF_REC % 16 == 0, "16-B aligned records");
+constexpr int OFF_PART = OFF_REC + NW * 32 * REC * 4;          // float2 [NW][GN][32]: lane partials
+constexpr int OFF_MD = OFF_PART + NW * GN * 32 * 8;            // uint8 [NW][32]: (column << 3) | z offset
+constexpr int SMEM = OFF_MD + NW * 32 + 32;   // (+32: md reads run one pair past a batch)
+static_assert(OFF_REC % 16 == 0 && OFF_PART % 16 == 0, "16-B aligned records and partials");
+static_assert(SMEM + 256 <= 227 * 1024, "shared memory per CTA");
 
 }  // namespace g3y
 
@@ -154,18 +157,19 @@ __device__ __forceinline__ void g3y_kron(const float u, float (&w)[8]) {
 
 // Phase B: records of sorted nodes [s0, min(s0 + 32, e)) (lane k: node s0 + k; the sort key's minor
 // digit puts an x-line's nodes in y-column order): the 24 tap weights (tap polynomials, R1), the y
-// weights as the pairs each row-lane group needs at the node's column, (column, z offset) and the
-// destination.  All lanes evaluate taps (idle lanes on u = 1/2) so that the rare Kronecker fix-up is a
-// warp vote.
+// weights as the pairs each row-lane group needs at the node's column, and the byte (column, z
+// offset).  All lanes evaluate taps (idle lanes on u = 1/2) so that the rare Kronecker fix-up is a warp
+// vote; idle lanes write a record at the last node's cell (the node loop runs in pairs and may touch
+// one of them; its value is never stored).  Returns the lane's destination index.
 template <bool POLY>
-__device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32_t s0, uint32_t e, float* rec,
-                                            int lane, const float4 c4, const uint32_t pj) {
+__device__ __forceinline__ uint32_t g3y_phase_b(const GatherParams<float>& p, uint32_t s0, uint32_t e, float* rec,
+                                                uint8_t* mdb, int lane, const float4 c4, const uint32_t pj) {
   constexpr int T = g3y::T;
   const uint32_t i = s0 + (uint32_t)lane;
   const bool act = i < e;
   float w[3][T];
+  const float uu[3] = {act ? c4.x : 0.5f, act ? c4.y : 0.5f, act ? c4.z : 0.5f};
   if (POLY) {
-    const float uu[3] = {act ? c4.x : 0.5f, act ? c4.y : 0.5f, act ? c4.z : 0.5f};
 #ifdef G3Y_ABL_NOTAPS
     for (int t = 0; t < 3; ++t)
       for (int q = 0; q < T; ++q) w[t][q] = uu[0] * (float)(q + t);
@@ -180,45 +184,90 @@ __device__ __forceinline__ void g3y_phase_b(const GatherParams<float>& p, uint32
       for (int t = 0; t < 3; ++t) g3y_kron(uu[t], w[t]);
     }
 #endif
-  } else if (act) {
-    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.x, p), p, w[0]);
-    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.y, p), p, w[1]);
-    all_taps<T, POLY>(dim_state<T, float, POLY>((double)c4.z, p), p, w[2]);
+  } else {
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)uu[0], p), p, w[0]);
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)uu[1], p), p, w[1]);
+    all_taps<T, POLY>(dim_state<T, float, POLY>((double)uu[2], p), p, w[2]);
   }
-  if (act) {
-    const uint32_t md = __float_as_uint(c4.w);
-    const int col = (int)(md >> 3);
-    float* r = rec + lane * g3y::REC;
-    reinterpret_cast<float4*>(r)[2] = make_float4(w[1][0], w[1][1], w[1][2], w[1][3]);
-    reinterpret_cast<float4*>(r)[3] = make_float4(w[1][4], w[1][5], w[1][6], w[1][7]);
-    // row-lane group q holds window rows b = (q - col) & 7 and b ^ 4: pairs (wy[b], wy[b ^ 4])
-    float yq[8];
+  uint32_t md = __float_as_uint(c4.w);
+  md = __shfl_sync(0xffffffffu, md, act ? lane : (int)(e - 1u - s0));
+  const int col = (int)(md >> 3);
+  float* r = rec + lane * g3y::REC;
+  reinterpret_cast<float4*>(r)[2] = make_float4(w[1][0], w[1][1], w[1][2], w[1][3]);
+  reinterpret_cast<float4*>(r)[3] = make_float4(w[1][4], w[1][5], w[1][6], w[1][7]);
+  // row-lane group q holds window rows b = (q - col) & 7 and b ^ 4: pairs (wy[b], wy[b ^ 4])
+  float yq[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int b = (q - col) & 7;
-      yq[2 * q] = r[8 + b];
-      yq[2 * q + 1] = r[8 + (b ^ 4)];
-    }
-    reinterpret_cast<float4*>(r)[2] = make_float4(yq[0], yq[1], yq[2], yq[3]);
-    reinterpret_cast<float4*>(r)[3] = make_float4(yq[4], yq[5], yq[6], yq[7]);
-    reinterpret_cast<float4*>(r)[0] = make_float4(w[2][0], w[2][1], w[2][2], w[2][3]);
-    reinterpret_cast<float4*>(r)[1] = make_float4(w[2][4], w[2][5], w[2][6], w[2][7]);
-    reinterpret_cast<float4*>(r)[4] = make_float4(w[0][0], w[0][1], w[0][2], w[0][3]);
-    reinterpret_cast<float4*>(r)[5] = make_float4(w[0][4], w[0][5], w[0][6], w[0][7]);
-    reinterpret_cast<uint2*>(r)[12] = make_uint2(md, p.sorted_out ? i : pj);
+  for (int q = 0; q < 4; ++q) {
+    const int b = (q - col) & 7;
+    yq[2 * q] = r[8 + b];
+    yq[2 * q + 1] = r[8 + (b ^ 4)];
   }
+  reinterpret_cast<float4*>(r)[2] = make_float4(yq[0], yq[1], yq[2], yq[3]);
+  reinterpret_cast<float4*>(r)[3] = make_float4(yq[4], yq[5], yq[6], yq[7]);
+  reinterpret_cast<float4*>(r)[0] = make_float4(w[2][0], w[2][1], w[2][2], w[2][3]);
+  reinterpret_cast<float4*>(r)[1] = make_float4(w[2][4], w[2][5], w[2][6], w[2][7]);
+  reinterpret_cast<float4*>(r)[4] = make_float4(w[0][0], w[0][1], w[0][2], w[0][3]);
+  reinterpret_cast<float4*>(r)[5] = make_float4(w[0][4], w[0][5], w[0][6], w[0][7]);
+  mdb[lane] = (uint8_t)md;
   __syncwarp();
+  return p.sorted_out ? i : pj;
 }
 
-// the lane's 16 z values of box row (x-plane xa, row r) into a slot
-__device__ __forceinline__ void g3y_load_row(const float2* box, int xa, int r, float2 (&R)[16]) {
-  const float4* src = reinterpret_cast<const float4*>(box + (xa * g3y::BY + r) * g3y::BZ);
+// Shared-memory accesses of the node loop by 32-bit shared address (kept in registers; volatile asm
+// so that the loads stay where they are written: the loop is latency-bound and the load placement is
+// its schedule).
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+
+// the lane's z values 1..15 of the box row at shared address a into a slot (value 0 of a row is never
+// a tap: z offsets start at box index 1)
+__device__ __forceinline__ void g3y_load_row(uint32_t a, float2 (&R)[16]) {
+  R[1] = lds64(a + 8);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float4 v = src[k];
+  for (int k = 1; k < 8; ++k) {
+    const float4 v = lds128(a + 16 * k);
     R[2 * k] = make_float2(v.x, v.y);
     R[2 * k + 1] = make_float2(v.z, v.w);
   }
+}
+// the same under a lane predicate (no divergent branch: the window advance of one lane group)
+__device__ __forceinline__ void g3y_load_row_if(uint32_t a, int pred, float2 (&R)[16]) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.s32 p, %15, 0;\n"
+      "@p ld.shared.v2.f32 {%0, %1}, [%14+8];\n"
+      "@p ld.shared.v4.f32 {%2, %3, %4, %5}, [%14+16];\n"
+      "@p ld.shared.v4.f32 {%6, %7, %8, %9}, [%14+32];\n"
+      "@p ld.shared.v4.f32 {%10, %11, %12, %13}, [%14+48];\n}"
+      : "+f"(R[1].x), "+f"(R[1].y), "+f"(R[2].x), "+f"(R[2].y), "+f"(R[3].x), "+f"(R[3].y), "+f"(R[4].x),
+        "+f"(R[4].y), "+f"(R[5].x), "+f"(R[5].y), "+f"(R[6].x), "+f"(R[6].y), "+f"(R[7].x), "+f"(R[7].y)
+      : "r"(a), "r"(pred));
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.s32 p, %17, 0;\n"
+      "@p ld.shared.v4.f32 {%0, %1, %2, %3}, [%16+64];\n"
+      "@p ld.shared.v4.f32 {%4, %5, %6, %7}, [%16+80];\n"
+      "@p ld.shared.v4.f32 {%8, %9, %10, %11}, [%16+96];\n"
+      "@p ld.shared.v4.f32 {%12, %13, %14, %15}, [%16+112];\n}"
+      : "+f"(R[8].x), "+f"(R[8].y), "+f"(R[9].x), "+f"(R[9].y), "+f"(R[10].x), "+f"(R[10].y), "+f"(R[11].x),
+        "+f"(R[11].y), "+f"(R[12].x), "+f"(R[12].y), "+f"(R[13].x), "+f"(R[13].y), "+f"(R[14].x), "+f"(R[14].y),
+        "+f"(R[15].x), "+f"(R[15].y)
+      : "r"(a), "r"(pred));
 }
 
 // z-dots of both slots for a node with z offset OZ (taps at box z index OZ + 1 + c); two partial
@@ -280,6 +329,8 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int la = lane & 7, lq = lane >> 3;
   float* const rec = reinterpret_cast<float*>(g3y_smem + OFF_REC) + wid * 32 * REC;
+  float2* const part = reinterpret_cast<float2*>(g3y_smem + OFF_PART) + wid * GN * 32;
+  uint8_t* const mdb = g3y_smem + OFF_MD + wid * 32;
   float2* __restrict__ out = (float2*)p.out;
   const uint32_t G = gridDim.x;
   const uint32_t nvirt = (uint32_t)p.nkeys_morton;
@@ -342,7 +393,8 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
     const uint32_t nb0 = cur.b0, ne = cur.e0;
     const float2* box = boxes + (size_t)b * (BOXB / 8);
     const int xa = cur.w + la;       // box x index of the lane's rows
-    if (nb0 < ne) g3y_phase_b<POLY>(p, nb0, ne, rec, lane, c4, pj);   // overlaps the box's TMA
+    uint32_t dst = 0;
+    if (nb0 < ne) dst = g3y_phase_b<POLY>(p, nb0, ne, rec, mdb, lane, c4, pj);   // overlaps the box's TMA
     else if (nxt.b0 < nxt.e0) g3y_fetch(p, nxt.b0, nxt.e0, lane, c4, pj);
     while (s_tag[b] != (int)k) {
     }
@@ -350,24 +402,28 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
     if (nb0 < ne) {
       // ---- sweep: nodes in column order; the row window starts at the first node's column
       float2 R0[16], R1[16];
-      int ycur = (int)(reinterpret_cast<const uint32_t*>(rec)[24] >> 3);
-      g3y_load_row(box, xa, ycur + ((lq - ycur) & 7), R0);
-      g3y_load_row(box, xa, ycur + ((lq + 4 - ycur) & 7), R1);
+      const uint32_t rec_s = smem_u32(rec), mdb_s = smem_u32(mdb);
+      // the lane's x-plane of the box (rows of 144 B)
+      uint32_t row_s = smem_u32(box) + (uint32_t)(xa * (BY * BZ * 8));
+      int lqo = lq;   // (opaque copies: kept in registers instead of being recomputed in the loop)
+      asm volatile("" : "+r"(row_s), "+r"(lqo));
+      int ycur = (int)(lds8(mdb_s) >> 3);
+      g3y_load_row(row_s + (uint32_t)(ycur + ((lq - ycur) & 7)) * (BZ * 8), R0);
+      g3y_load_row(row_s + (uint32_t)(ycur + ((lq + 4 - ycur) & 7)) * (BZ * 8), R1);
       for (uint32_t s0 = nb0;;) {
         const int nq = (int)min(32u, ne - s0);
         if (s0 + 32 < ne) g3y_fetch(p, s0 + 32, ne, lane, c4, pj);   // next batch, in flight meanwhile
         else if (nxt.b0 < nxt.e0) g3y_fetch(p, nxt.b0, nxt.e0, lane, c4, pj);   // the next slot's first batch
-        // Nodes are processed in pairs whose instruction streams interleave: node B's record loads,
-        // window advance and z-dots issue while node A's shuffle sum is in flight (the per-node chain
-        // of dependent shared-memory loads, branches and shuffles is the kernel's critical path).
         auto advance = [&](int col) {
-          while (ycur < col) {   // window [ycur, ycur + 8) -> [ycur + 1, ycur + 9): row ycur + 8
-            const int rn = ycur + 8;
-            if (lq == (rn & 3)) {
-              if ((rn >> 2) & 1) g3y_load_row(box, xa, rn, R1);
-              else g3y_load_row(box, xa, rn, R0);
-            }
-            ++ycur;
+          if (ycur < col) {
+#pragma unroll 1
+            do {   // window [ycur, ycur + 8) -> [ycur + 1, ycur + 9): row ycur + 8
+              const int rn = ycur + 8;
+              const uint32_t a = row_s + (uint32_t)rn * (BZ * 8);
+              const int mine = lqo == (rn & 3);
+              if (rn & 4) g3y_load_row_if(a, mine, R1);
+              else g3y_load_row_if(a, mine, R0);
+            } while (++ycur < col);
           }
         };
         auto zdot = [&](uint32_t oz, const float4& wa, const float4& wb, float2& d0, float2& d1) {
@@ -382,78 +438,68 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
             default: g3y_zdot<7>(R0, R1, wa, wb, d0, d1); break;
           }
         };
-        // y contraction of the lane's two rows (then summed over the 4 row lanes of x-plane a; the
-        // x-plane sums overwrite the node's consumed z and y weights)
-        auto ycon = [&](const float2& wy, const float2& d0, const float2& d1) {
-          float2 t = __fmul2_rn(make_float2(wy.x, wy.x), d0);
-          cmac(t, wy.y, d1);
-          return t;
-        };
-        auto shfl2 = [&](const float2& t, int o) {
-          return make_float2(__shfl_xor_sync(0xffffffffu, t.x, o), __shfl_xor_sync(0xffffffffu, t.y, o));
-        };
-        const bool odd_q = (lq & 1) != 0;
-        float* r = rec;
-        int q = 0;
-        for (; q + 1 < nq; q += 2, r += 2 * REC) {
-          float* rB = r + REC;
-          const uint32_t mdA = reinterpret_cast<const uint32_t*>(r)[24];
-          const uint32_t mdB = reinterpret_cast<const uint32_t*>(rB)[24];
-          const float4 waA = reinterpret_cast<const float4*>(r)[0];
-          const float4 wbA = reinterpret_cast<const float4*>(r)[1];
-          const float2 wyA = reinterpret_cast<const float2*>(r + 8)[lq];
-          advance((int)(mdA >> 3));
-          float2 d0, d1;
-          zdot(mdA & 7u, waA, wbA, d0, d1);
-          const float2 tA = ycon(wyA, d0, d1);
-          const float4 waB = reinterpret_cast<const float4*>(rB)[0];
-          const float4 wbB = reinterpret_cast<const float4*>(rB)[1];
-          const float2 wyB = reinterpret_cast<const float2*>(rB + 8)[lq];
-          advance((int)(mdB >> 3));
-          zdot(mdB & 7u, waB, wbB, d0, d1);
-          const float2 tB = ycon(wyB, d0, d1);
-          // transposed sum over the 4 row lanes: lanes with even q keep node A, odd q node B, and
-          // receive their partner's share of it (the same additions, in the same order, as a
-          // butterfly per node: (q0 + q1) + (q2 + q3))
-          float2 kp = odd_q ? tB : tA;
-          const float2 sd = odd_q ? tA : tB;
-          kp = __fadd2_rn(kp, shfl2(sd, 8));
-          kp = __fadd2_rn(kp, shfl2(kp, 16));
-          if (lq < 2) reinterpret_cast<float2*>(lq ? rB : r)[la] = kp;
+        // Nodes run in pairs, groups of GN.  Per node: window advance to its column, the lane's two
+        // z-dots, their y contraction; the lane's share (x-plane a, row lanes q) goes to row j of the
+        // group's partial buffer.  Records are loaded ahead of use: the pair's second node during the
+        // first one's z-dots, the next pair's first node during the second one's.  After each group
+        // lane (n, h) = (lane >> 2, lane & 3) contracts node n's partials of x-planes 2h, 2h + 1 (all
+        // four row-lane groups) with wx, two shuffles add the four h, lanes h = 0 store (fixed
+        // order: bitwise reproducible).
+        uint32_t r_s = rec_s, ry_s = rec_s + 32 + 8 * lq, mq_s = mdb_s;   // running: record, y pair, md
+        uint32_t mdA = lds8(mq_s);
+        float4 waA = lds128(r_s), wbA = lds128(r_s + 16);
+        float2 wyA = lds64(ry_s);
+        for (int g0 = 0; g0 < nq; g0 += GN) {
+          uint32_t pp = smem_u32(part) + 8 * lane;
+          const uint32_t pe = pp + 256 * min(GN, (nq - g0 + 1) & ~1);
+#pragma unroll 1
+          do {
+            float2 d0, d1, t;
+            advance((int)(mdA >> 3));
+            zdot(mdA & 7u, waA, wbA, d0, d1);
+            const uint32_t mdB = lds8(mq_s + 1);
+            const float4 waB = lds128(r_s + 4 * REC), wbB = lds128(r_s + 4 * REC + 16);
+            const float2 wyB = lds64(ry_s + 4 * REC);
+            t = __fmul2_rn(make_float2(wyA.x, wyA.x), d0);
+            cmac(t, wyA.y, d1);
+            sts64(pp, t);
+            advance((int)(mdB >> 3));
+            zdot(mdB & 7u, waB, wbB, d0, d1);
+            mdA = lds8(mq_s + 2);          // (past the batch: unused)
+            waA = lds128(r_s + 8 * REC);
+            wbA = lds128(r_s + 8 * REC + 16);
+            wyA = lds64(ry_s + 8 * REC);
+            t = __fmul2_rn(make_float2(wyB.x, wyB.x), d0);
+            cmac(t, wyB.y, d1);
+            sts64(pp + 256, t);
+            pp += 512;
+            r_s += 8 * REC;
+            ry_s += 8 * REC;
+            mq_s += 2;
+          } while (pp != pe);
+          __syncwarp();
+          {
+            const int n = lane >> 2, h = lane & 3;
+            const float2 wx = lds64(rec_s + (uint32_t)((g0 + n) * (4 * REC) + 64 + 8 * h));
+            const uint32_t pr = smem_u32(part) + (uint32_t)(n * 256 + h * 16);
+            float2 f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 v = lds128(pr + 64 * i);
+              if (i == 0) f = __fmul2_rn(make_float2(wx.x, wx.x), make_float2(v.x, v.y));
+              else cmac(f, wx.x, make_float2(v.x, v.y));
+              cmac(f, wx.y, make_float2(v.z, v.w));
+            }
+            f = __fadd2_rn(f, make_float2(__shfl_xor_sync(0xffffffffu, f.x, 1), __shfl_xor_sync(0xffffffffu, f.y, 1)));
+            f = __fadd2_rn(f, make_float2(__shfl_xor_sync(0xffffffffu, f.x, 2), __shfl_xor_sync(0xffffffffu, f.y, 2)));
+            const uint32_t d = __shfl_sync(0xffffffffu, dst, g0 + n);
+            if (h == 0 && g0 + n < nq) out[d] = f;
+          }
+          __syncwarp();   // partial buffer free for the next group
         }
-        if (q < nq) {   // odd node
-          const uint32_t md = reinterpret_cast<const uint32_t*>(r)[24];
-          const float4 wa = reinterpret_cast<const float4*>(r)[0];
-          const float4 wb = reinterpret_cast<const float4*>(r)[1];
-          const float2 wy = reinterpret_cast<const float2*>(r + 8)[lq];
-          advance((int)(md >> 3));
-          float2 d0, d1;
-          zdot(md & 7u, wa, wb, d0, d1);
-          float2 t = ycon(wy, d0, d1);
-          t = __fadd2_rn(t, shfl2(t, 8));
-          t = __fadd2_rn(t, shfl2(t, 16));
-          if (lq == 0) reinterpret_cast<float2*>(r)[la] = t;
-        }
-        __syncwarp();
-        // ---- x contraction and store: lane k finishes node s0 + k
-        if (lane < nq) {
-          const float4* rr = reinterpret_cast<const float4*>(rec + lane * REC);
-          const float4 v0 = rr[0], v1 = rr[1], v2 = rr[2], v3 = rr[3], wx0 = rr[4], wx1 = rr[5];
-          float2 f = __fmul2_rn(make_float2(wx0.x, wx0.x), make_float2(v0.x, v0.y));
-          cmac(f, wx0.y, make_float2(v0.z, v0.w));
-          cmac(f, wx0.z, make_float2(v1.x, v1.y));
-          cmac(f, wx0.w, make_float2(v1.z, v1.w));
-          cmac(f, wx1.x, make_float2(v2.x, v2.y));
-          cmac(f, wx1.y, make_float2(v2.z, v2.w));
-          cmac(f, wx1.z, make_float2(v3.x, v3.y));
-          cmac(f, wx1.w, make_float2(v3.z, v3.w));
-          const uint32_t d = reinterpret_cast<const uint32_t*>(rec + lane * REC)[25];
-          out[d] = f;
-        }
-        __syncwarp();   // records free for the next batch
         s0 += 32;
         if (s0 >= ne) break;
-        g3y_phase_b<POLY>(p, s0, ne, rec, lane, c4, pj);
+        dst = g3y_phase_b<POLY>(p, s0, ne, rec, mdb, lane, c4, pj);
       }
     }
     // ---- release box buffer b; the warp completing the item's eighth x-line loads item k + NBUF
