@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-peaks", action="store_true")
+    ap.add_argument("--one-call", action="store_true",
+                    help="step = bnfft_transform (grid stage concurrent with the sort) instead of "
+                         "precompute + set_nodes + execute; measured equal on cfg4 (both HBM-bound), -5 %% on cfg2")
     ap.add_argument("--dist", default="auto", choices=["auto", "slab", "replicas"],
                     help="N>1: slab = one problem split over the ranks (d = 3), replicas = one per rank")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -318,11 +321,14 @@ def make_plan(bn, cfg, prec, window, device, stream, dist_kw=None):
                    device=device, stream=stream.cuda_stream, **(dist_kw or {}))
 
 
-def time_steps(torch, plan, x_dev, fh_dev, out, steps, warmup, stream, world=1, dist=None):
+def time_steps(torch, plan, x_dev, fh_dev, out, steps, warmup, stream, world=1, dist=None, three_calls=True):
     def step():
-        plan.precompute()
-        plan.set_nodes(x_dev)
-        plan.execute(fh_dev, out)
+        if three_calls:
+            plan.precompute()
+            plan.set_nodes(x_dev)
+            plan.execute(fh_dev, out)
+        else:   # the same work in one call: the grid stage overlaps the node sort (bnfft_transform)
+            plan.transform(x_dev, fh_dev, out)
 
     for _ in range(warmup):
         step()
@@ -392,7 +398,7 @@ def run_config(torch, bn, cfg, prec, window, steps, warmup, dev, local, stream, 
     fh_dev = torch.from_numpy(fh_np).to(dev)
     plan = make_plan(bn, cfg, prec, window, local, stream, dist_kw)
     out = torch.empty((cfg.batch, x_np.shape[0]), dtype=plan.cdtype, device=dev)
-    ms_total = time_steps(torch, plan, x_dev, fh_dev, out, steps, warmup, stream, world, dist)
+    ms_total = time_steps(torch, plan, x_dev, fh_dev, out, steps, warmup, stream, world, dist, THREE_CALLS)
     tm = plan.timing()
     info = plan.info()
     stages = {k: getattr(tm, "ms_" + k) / steps for k in STAGES}
@@ -418,7 +424,12 @@ def summary(cfg, prec, window, res, steps, peaks):
     }
 
 
+THREE_CALLS = True
+
+
 def run_gpu(args):
+    global THREE_CALLS
+    THREE_CALLS = not args.one_call
     import torch
     import torch.distributed as dist
 
@@ -476,6 +487,9 @@ def run_gpu(args):
                                         f"exchange)") if slab else f"replicas{world}"),
             "roofline": s["roofline"],
             "stages_ms": s["stages_ms"],
+            "step_api": ("bnfft_precompute + bnfft_set_nodes + bnfft_execute" if THREE_CALLS else
+                         "bnfft_transform (psi^, deconvolution and iFFT on the plan's side stream, "
+                         "concurrent with keys + sort + build; stage times overlap)"),
             "product_nodes_per_s": s["product_nodes_per_s"],
             "product_note": "keys + sort + build + deconv + gather (cuFFT and psi^ excluded)",
             "gather_nodes_per_s": s["gather_nodes_per_s"],

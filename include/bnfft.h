@@ -217,6 +217,18 @@ BNFFT_API int bnfft_set_nodes(struct bnfft_plan_s* plan, int64_t n, const double
  * asynchronous; errors of earlier asynchronous work surface as BNFFT_E_CUDA. */
 BNFFT_API int bnfft_execute(struct bnfft_plan_s* plan, const void* fhat_dev, void* f_dev);
 
+/* Algorithm 2 in one call on device buffers: step 0(a), row a1 (bnfft_set_nodes) and
+ * steps 1-3 (bnfft_execute) for n nodes x_dev, spectrum fhat_dev, values into f_dev (layouts as in
+ * those calls).  Steps 0(a), 1 and 2 do not depend on the nodes, and the bin sort does not depend on
+ * f^: they run concurrently, the grid stage on the plan's side stream (forked from the plan's stream
+ * at the call, so everything enqueued earlier on the plan's stream is visible to both), the sort on
+ * the plan's stream; step 3 joins them.  Results are bitwise equal to precompute + set_nodes +
+ * execute.  Synchronous up to the node validation (as bnfft_set_nodes); the gather is asynchronous
+ * on the plan's stream.  Errors and first_bad as bnfft_set_nodes / bnfft_execute.  Multi-rank plans
+ * run the three calls in sequence. */
+BNFFT_API int bnfft_transform(struct bnfft_plan_s* plan, int64_t n, const double* x_dev, const void* fhat_dev,
+                              void* f_dev, int64_t* first_bad);
+
 /* Step 3 alone with caller-provided grid samples: f_j = sum_{l in I_L} s_l psi(x_j - l/L), i.e. the
  * regularized Shannon sampling formula with localized sampling (eq. Rmf(x)_multi) restricted
  * to l in I_L (first equality of P:463); with BNFFT_ALG1 the periodic sum with the window,

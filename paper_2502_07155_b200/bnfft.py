@@ -90,6 +90,7 @@ _sig = {
     "bnfft_precompute": (c_int, [_P]),
     "bnfft_set_nodes": (c_int, [_P, c_int64, c_void_p, POINTER(c_int64)]),
     "bnfft_execute": (c_int, [_P, c_void_p, c_void_p]),
+    "bnfft_transform": (c_int, [_P, c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_int64)]),
     "bnfft_transform_host": (c_int, [_P, c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_int64)]),
     "bnfft_transform_host_many": (c_int, [_P, c_int32, c_int64, POINTER(c_void_p), POINTER(c_void_p),
                                           POINTER(c_void_p), POINTER(c_int64)]),
@@ -204,6 +205,27 @@ class Plan:
             out = t.empty((self.batch, self.n), dtype=self.cdtype, device=fhat.device)
         self._check_out(out)
         check(bnfft_execute(self.h, _ptr(fhat), _ptr(out) if (self.n or self.slab) else None), "bnfft_execute")
+        return out
+
+    def transform(self, x, fhat, out=None):
+        """Algorithm 2 in one call (bnfft_transform): the grid stage overlaps the node sort."""
+        t = self._torch
+        assert x.dtype == t.float64 and x.is_cuda and x.is_contiguous()
+        assert fhat.dtype == self.cdtype and fhat.is_cuda and fhat.is_contiguous()
+        assert fhat.numel() == self.batch * self.M ** self.d
+        n = x.shape[0]
+        if out is None:
+            out = t.empty((self.batch, n), dtype=self.cdtype, device=fhat.device)
+        self.n_user = n
+        self.n = n
+        self._check_out(out)
+        bad = c_int64(-1)
+        code = bnfft_transform(self.h, n, _ptr(x) if n else None, _ptr(fhat),
+                               _ptr(out) if (n or self.slab) else None, ctypes.byref(bad))
+        if code != BNFFT_OK:
+            err = BnfftError(code, "bnfft_transform")
+            err.first_bad = bad.value
+            raise err
         return out
 
     def interpolate(self, samples, out=None):

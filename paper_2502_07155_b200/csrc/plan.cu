@@ -661,17 +661,9 @@ int bnfft::local_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t*
   return BNFFT_OK;
 }
 
-extern "C" {
-
-int bnfft_execute(bnfft_plan_s* p, const void* fhat, void* f) {
-  if (!p) return BNFFT_E_INVALID_ARG;
-  if (!p->nodes_set) { set_error("call bnfft_set_nodes first"); return BNFFT_E_NODES_NOT_SET; }
-  const int64_t n_out = (p->dist && p->opts.dist == BNFFT_DIST_SLAB) ? 1 : p->n;
-  if (!fhat || (n_out > 0 && !f)) { set_error("NULL buffer"); return BNFFT_E_INVALID_ARG; }
-  cudaSetDevice(p->device);
+// Steps 1 and 2 (deconvolution + zero-pad, inverse FFT) on p->stream: theta into d_grid
+static int grid_stage(bnfft_plan_s* p, const void* fhat) {
   cudaError_t e;
-  if ((e = join_precompute(p)) != cudaSuccess) return cuda_fail(e, "precompute join");
-  if (p->dist && p->opts.dist == BNFFT_DIST_SLAB) return dist_execute(p, fhat, f);
   cudaEvent_t ev;
   timer_begin(p, ST_DECONV, &ev);
   if ((e = launch_deconv(p, fhat)) != cudaSuccess) return cuda_fail(e, "deconv kernel");
@@ -699,6 +691,64 @@ int bnfft_execute(bnfft_plan_s* p, const void* fhat, void* f) {
     return BNFFT_E_CUFFT;
   }
   timer_end(p, ST_FFT, ev);
+  return BNFFT_OK;
+}
+
+extern "C" {
+
+int bnfft_execute(bnfft_plan_s* p, const void* fhat, void* f) {
+  if (!p) return BNFFT_E_INVALID_ARG;
+  if (!p->nodes_set) { set_error("call bnfft_set_nodes first"); return BNFFT_E_NODES_NOT_SET; }
+  const int64_t n_out = (p->dist && p->opts.dist == BNFFT_DIST_SLAB) ? 1 : p->n;
+  if (!fhat || (n_out > 0 && !f)) { set_error("NULL buffer"); return BNFFT_E_INVALID_ARG; }
+  cudaSetDevice(p->device);
+  cudaError_t e;
+  if ((e = join_precompute(p)) != cudaSuccess) return cuda_fail(e, "precompute join");
+  if (p->dist && p->opts.dist == BNFFT_DIST_SLAB) return dist_execute(p, fhat, f);
+  int rc = grid_stage(p, fhat);
+  if (rc != BNFFT_OK) return rc;
+  cudaEvent_t ev;
+  timer_begin(p, ST_GATHER, &ev);
+  if ((e = launch_gather(p, f)) != cudaSuccess) return cuda_fail(e, "gather kernel");
+  timer_end(p, ST_GATHER, ev);
+  p->n_exec++;
+  return BNFFT_OK;
+}
+
+/* One call for the whole of Algorithm 2 on device buffers (header: bnfft_transform). */
+int bnfft_transform(bnfft_plan_s* p, int64_t n, const double* x, const void* fhat, void* f, int64_t* first_bad) {
+  if (first_bad) *first_bad = -1;
+  if (!p) return BNFFT_E_INVALID_ARG;
+  if (n < 0 || n >= ((int64_t)1 << 31) || (n > 0 && !x) || !fhat || (n > 0 && !f)) {
+    set_error("n must be in [0, 2^31), buffers non-NULL");
+    return BNFFT_E_INVALID_ARG;
+  }
+  cudaSetDevice(p->device);
+  int rc;
+  if (p->dist) {   // multi-rank plans: the exchange steps order the stages
+    if ((rc = bnfft_precompute(p)) != BNFFT_OK) return rc;
+    if ((rc = bnfft_set_nodes(p, n, x, first_bad)) != BNFFT_OK) return rc;
+    return bnfft_execute(p, fhat, f);
+  }
+  // fork: steps 0(a), 1, 2 on the side stream (they do not depend on the nodes) ...
+  if ((rc = bnfft_precompute(p)) != BNFFT_OK) return rc;
+  cudaStream_t main_stream = p->stream;
+  cufftResult fr = cufftSetStream(p->fft, p->pre_stream);
+  if (fr == CUFFT_SUCCESS && p->pfft3) fr = cufftSetStream(p->fft2, p->pre_stream);
+  if (fr != CUFFT_SUCCESS) { set_error("cufftSetStream failed"); return BNFFT_E_CUFFT; }
+  p->stream = p->pre_stream;
+  rc = grid_stage(p, fhat);
+  p->stream = main_stream;
+  cudaError_t e = cudaEventRecord(p->ev_pre, p->pre_stream);   // the join now covers the grid stage
+  fr = cufftSetStream(p->fft, main_stream);
+  if (fr == CUFFT_SUCCESS && p->pfft3) fr = cufftSetStream(p->fft2, main_stream);
+  if (rc != BNFFT_OK) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "transform join");
+  if (fr != CUFFT_SUCCESS) { set_error("cufftSetStream failed"); return BNFFT_E_CUFFT; }
+  // ... while row a1 (validate, sort, offsets) runs on the plan's stream
+  if ((rc = local_set_nodes(p, n, x, first_bad)) != BNFFT_OK) return rc;   // (a bad node: the join stays pending)
+  if ((e = join_precompute(p)) != cudaSuccess) return cuda_fail(e, "transform join");
+  cudaEvent_t ev;
   timer_begin(p, ST_GATHER, &ev);
   if ((e = launch_gather(p, f)) != cudaSuccess) return cuda_fail(e, "gather kernel");
   timer_end(p, ST_GATHER, ev);

@@ -222,6 +222,41 @@ def test_transform_host_matches_device(bn, torch):
     plan.close()
 
 
+@pytest.mark.parametrize("d,M,m,prec,N", [(1, 1 << 12, 8, "c64", 50_000), (3, 32, 4, "c64", 60_000),
+                                           (2, 64, 5, "c128", 30_000)])
+def test_transform_one_call(bn, torch, d, M, m, prec, N):
+    """bnfft_transform (grid stage on the side stream, concurrent with the sort): bitwise equal to
+    precompute + set_nodes + execute, over repeated calls with changing nodes and spectra; a bad
+    node is reported and the plan stays usable."""
+    cfg = synth.CONFIGS[{1: 2, 2: 3, 3: 4}[d]].scaled(M=M, N=N)
+    dev = torch.device("cuda:0")
+    cd = np.complex128 if prec == "c128" else np.complex64
+    plan = bn.Plan(d, M, 2.0, m, "sinh", prec)
+    ref_plan = bn.Plan(d, M, 2.0, m, "sinh", prec)
+    for v in range(3):
+        x = synth.make_nodes(cfg, variant=v)[: N - 1000 * v]
+        fh = synth.make_spectrum(cfg, variant=v, prec=prec).astype(cd)
+        xt = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        ft = torch.from_numpy(np.ascontiguousarray(fh)).to(dev)
+        f1 = plan.transform(xt, ft)
+        ref_plan.precompute()
+        ref_plan.set_nodes(xt)
+        f2 = ref_plan.execute(ft)
+        assert torch.equal(f1, f2)
+        if v == 0:
+            ref = oracle_f(x, fh, M, 2.0, m, "sinh")
+            assert rel_l2(f1.cpu().numpy(), ref["f"]) <= TOL[prec]
+    xb = x.copy()
+    xb[123] = 0.75
+    with pytest.raises(bn.BnfftError) as ei:
+        plan.transform(torch.from_numpy(xb).to(dev), ft)
+    assert ei.value.first_bad == 123
+    f1 = plan.transform(xt, ft)
+    assert torch.equal(f1, f2)
+    plan.close()
+    ref_plan.close()
+
+
 @pytest.mark.parametrize("d,M,m,prec", [(1, 1 << 10, 8, "c64"), (3, 16, 4, "c64"), (2, 32, 5, "c128")])
 def test_transform_host_many_pipelined(bn, torch, d, M, m, prec):
     """bnfft_transform_host_many: five steps with different node sets and spectra, each equal bitwise
