@@ -189,6 +189,8 @@ void set_error(const std::string& s);
 int cuda_fail(cudaError_t e, const char* what);
 
 // timing helpers
+// SM count of the current device (cached per device): grid-stride launch caps are multiples of it
+int sm_count();
 void timer_begin(bnfft_plan_s* p, int stage, cudaEvent_t* ev);
 void timer_end(bnfft_plan_s* p, int stage, cudaEvent_t ev);
 

@@ -42,7 +42,7 @@ __global__ void deconv_kernel(const C* __restrict__ fhat, C* __restrict__ X,
 cudaError_t launch_deconv(bnfft_plan_s* p, const void* fhat) {
   int64_t total = p->Md * p->opts.batch;
   if (total == 0) return cudaSuccess;
-  int64_t blocks = std::min<int64_t>((total + 255) / 256, 148LL * 32);
+  int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 32);
   void* X = p->pfft3 ? p->d_fft_p : p->d_fft_in;
   const int64_t L0 = p->pfft3 ? p->opts.M : p->L;
   if (p->c128)
@@ -87,7 +87,7 @@ __global__ void deconv_slab_kernel(const C* __restrict__ fhat, C* __restrict__ X
 cudaError_t launch_deconv_slab(bnfft_plan_s* p, const void* fhat, void* out, int64_t k0_lo, int64_t k0_hi) {
   const int64_t total = (k0_hi - k0_lo) * p->opts.M * p->opts.M;
   if (total <= 0) return cudaSuccess;
-  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148LL * 32);
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 32);
   if (p->c128)
     deconv_slab_kernel<double2, double><<<(unsigned)blocks, 256, 0, p->stream>>>(
         (const double2*)fhat, (double2*)out, p->d_q, p->opts.M, p->L, k0_lo, total);

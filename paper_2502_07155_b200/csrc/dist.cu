@@ -640,7 +640,7 @@ int dist_set_nodes(bnfft_plan_s* p, int64_t n, const double* x, int64_t* first_b
     if ((e = cudaMemsetAsync(ds->d_hist, 0, L * sizeof(unsigned long long), s)) != cudaSuccess)
       return cuda_fail(e, "zero histogram");
     if (n > 0) {
-      dist_plane_hist_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, L * sizeof(unsigned), s>>>(
+      dist_plane_hist_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 8), 256, L * sizeof(unsigned), s>>>(
           x, n, d, (double)L, L, ds->d_hist);
       p->launches++;
     }
@@ -906,7 +906,7 @@ int dist_execute(bnfft_plan_s* p, const void* fhat, void* f) {
     }
     if ((rc = ds->tr->exchange(rops, s)) != BNFFT_OK) return rc;
     if (ds->n_user > 0) {
-      const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(ds->n_user, 256), 148 * 16);
+      const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(ds->n_user, 256), (int64_t)sm_count() * 16);
       if (p->c128)
         dist_unpermute_kernel<double2><<<blocks, 256, 0, s>>>((const double2*)ds->d_fret, ds->d_sendperm, ds->n_user,
                                                               (double2*)f);

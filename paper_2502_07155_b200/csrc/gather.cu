@@ -18,6 +18,8 @@ const void* gather3y_kernel_ptr(bool poly);
 size_t gather3y_smem();
 int gather3y_threads();
 void gather3y_box(int* ext);
+const void* gather3q_kernel_ptr(bool poly);
+size_t gather3q_smem();
 void gather3y_item_table(int64_t nX, int64_t nY, int64_t nZ, std::vector<uint32_t>& tab);
 
 // d = 3, m = 4, complex64, batch 1: a specialised kernel chosen at plan creation (p->g3_kind) -- the
@@ -28,9 +30,10 @@ static bool use_coop3(const bnfft_plan_s* p) {
   return p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
 }
 static bool use_sweep3(const bnfft_plan_s* p) { return use_coop3(p) && p->g3_kind == 2; }
-static bool use_ysweep3(const bnfft_plan_s* p) { return use_coop3(p) && p->g3_kind == 0; }
+static bool use_ysweep3(const bnfft_plan_s* p) { return use_coop3(p) && (p->g3_kind == 0 || p->g3_kind == 3); }
 static const void* coop3_kernel(const bnfft_plan_s* p) {
   if (p->g3_kind == 0) return gather3y_kernel_ptr(p->tap_poly);
+  if (p->g3_kind == 3) return gather3q_kernel_ptr(p->tap_poly);
   if (p->g3_kind == 2) return gather3s_kernel_ptr(p->tap_poly);
   return p->tap_poly ? gather3c_kernel_p() : gather3c_kernel_e();
 }
@@ -99,7 +102,7 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   p->gather_box_elems = (int)box_elems;
   p->gather_bufstride = (int)(buf_bytes / p->csize);
   for (int t = 0; t < 3; ++t) p->gather_tbox[t] = t < d ? ext[t] : 1;
-  p->gather_smem = use_sweep3(p) ? gather3s_smem() : use_ysweep3(p) ? gather3y_smem() : nbuf * buf_bytes;
+  p->gather_smem = use_sweep3(p) ? gather3s_smem() : use_ysweep3(p) ? (p->g3_kind == 3 ? gather3q_smem() : gather3y_smem()) : nbuf * buf_bytes;
   p->gather_threads = use_sweep3(p) ? gather3s_threads() : use_ysweep3(p) ? gather3y_threads() : kGatherThreads;
   // tuning knob: 128-thread box CTAs (measured equal to 256 on cfg3: the kernel is latency-bound on
   // the node loads and box hand-offs, not on idle threads of sparse bins)
@@ -278,7 +281,7 @@ static cudaError_t launch_gather_t(bnfft_plan_s* p, void* out, const void* fn, b
   }
   void* args[] = {&gp};
   if (prepsi) {   // grid-stride elementwise kernel, no shared memory
-    unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p->n + kGatherThreads - 1) / kGatherThreads, 148 * 16));
+    unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p->n + kGatherThreads - 1) / kGatherThreads, (int64_t)sm_count() * 16));
     cudaError_t e3 = cudaLaunchKernel(fn, dim3(nb), dim3(kGatherThreads), args, 0, p->stream);
     p->launches++;
     return e3;

@@ -34,6 +34,19 @@ static cudaEvent_t get_event(bnfft_plan_s* p) {
   return e;
 }
 
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;   // B200
+    cached[dev] = n;
+  }
+  return cached[dev];
+}
+
 void timer_begin(bnfft_plan_s* p, int stage, cudaEvent_t* ev) {
   (void)stage;
   *ev = nullptr;
@@ -376,18 +389,18 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   // 1 x 16 x 8 cells; the half-warp / z-sweep kernels (gather3c / gather3s, selectable) use bins of
   // 8 x 8 x 16 cells (innermost box extent 16 + 2m = 24: conflict-free shared-memory rows).
   const bool coop3 = o->d == 3 && o->m == 4 && o->prec == BNFFT_C64 && o->batch == 1 && lgL >= 4;
-  p->g3_kind = getenv("BNFFT_GATHER3S") ? 2 : getenv("BNFFT_GATHER3C") ? 1 : 0;
-  if (p->g3_kind == 0 && L > 8192) p->g3_kind = 1;   // y-sweep item table: 10-bit item coordinates
-  p->rec3 = coop3 && p->g3_kind == 0;
+  p->g3_kind = getenv("BNFFT_GATHER3S") ? 2 : getenv("BNFFT_GATHER3C") ? 1 : getenv("BNFFT_GATHER3Q") ? 3 : 0;
+  if ((p->g3_kind == 0 || p->g3_kind == 3) && L > 8192) p->g3_kind = 1;   // y-sweep item table: 10-bit item coordinates
+  p->rec3 = coop3 && (p->g3_kind == 0 || p->g3_kind == 3);
   for (int t = 0; t < 3; ++t) {
     int lt = lg;
-    if (coop3) lt = p->g3_kind == 0 ? (t == 0 ? 0 : t == 1 ? 4 : 3) : (t == 2 ? 4 : 3);
+    if (coop3) lt = p->rec3 ? (t == 0 ? 0 : t == 1 ? 4 : 3) : (t == 2 ? 4 : 3);
     p->bin_log2[t] = t < o->d ? lt : 0;
     p->nb_dim[t] = t < o->d ? (L + (1 << lt) - 1) >> lt : 1;
     nbins *= p->nb_dim[t];
   }
   p->nbins = nbins;
-  p->col_bits = p->rec3 ? 4 : 0;
+  p->col_bits = p->rec3 ? (p->g3_kind == 3 ? 5 : 4) : 0;
   p->key_bits = ceil_log2(nbins) + p->col_bits;
   p->sort_passes = (p->key_bits + kMaxDigitBits - 1) / kMaxDigitBits;
   p->digit_bits = p->sort_passes ? (p->key_bits + p->sort_passes - 1) / p->sort_passes : 0;
@@ -953,7 +966,8 @@ int bnfft_get_info(const bnfft_plan_s* p, bnfft_info* o) {
   } else {
     const bool coop3 = p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
     o->gather_kernel = !coop3 ? BNFFT_GK_BOX
-                       : p->g3_kind == 0 ? BNFFT_GK_YSWEEP3 : p->g3_kind == 1 ? BNFFT_GK_COOP3 : BNFFT_GK_SWEEP3;
+                       : p->g3_kind == 0 ? BNFFT_GK_YSWEEP3 : p->g3_kind == 3 ? BNFFT_GK_YSWEEP3Q
+                       : p->g3_kind == 1 ? BNFFT_GK_COOP3 : BNFFT_GK_SWEEP3;
   }
   return BNFFT_OK;
 }

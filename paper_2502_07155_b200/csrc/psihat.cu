@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256) psihat_kernel(const double* __restrict__ 
 cudaError_t launch_psihat(bnfft_plan_s* p) {
   int64_t M = p->opts.M;
   int64_t nrun = (M / 2 + 1 + kRun - 1) / kRun;
-  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((2 * nrun + 255) / 256, 148 * 8));
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((2 * nrun + 255) / 256, (int64_t)sm_count() * 8));
   unsigned long long init[2] = {0ull, 0x7fefffffffffffffull};   // 0.0, DBL_MAX
   cudaError_t e = cudaMemcpyAsync(p->d_flat, init, sizeof(init), cudaMemcpyHostToDevice, p->stream);
   if (e != cudaSuccess) return e;
@@ -161,7 +161,7 @@ __global__ void kernel_hat_kernel(const double* __restrict__ gl, const double* _
 
 cudaError_t launch_kernel_hat(bnfft_plan_s* p, const double* v_dev, double* out_dev, int64_t n) {
   if (n <= 0) return cudaSuccess;
-  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
   kernel_hat_kernel<<<blocks, 256, 0, p->stream>>>(p->d_gl, v_dev, out_dev, n, p->L, p->wp);
   p->launches++;
   return cudaGetLastError();

@@ -36,6 +36,12 @@ __device__ __forceinline__ int64_t hist_index(const SegLayout& sl, int64_t tile,
   return blk * sl.tpb * ndig + (int64_t)dg * tin + tib;
 }
 
+// rec3 plans: the minor key digit below the x-line bin.  colbits == 4 (gather3y): the y column c_1 mod 16;
+// colbits == 5 (gather3q): (half of the bin's z extent, y column) = ((c_2 >> 2) & 1) << 4 | c_1 mod 16.
+__device__ __forceinline__ uint32_t minor_digit(uint32_t cy, uint32_t cz, int colbits) {
+  return colbits == 5 ? ((((cz >> 2) & 1u) << 4) | (cy & 15u)) : (cy & ((1u << colbits) - 1u));
+}
+
 // K1: validate + key.  bad = min over nodes of (index << 4 | code).  Each thread handles a pair of
 // consecutive nodes with 16-byte loads/stores (2*D doubles, 2 keys).
 // The common case in one pass: all coordinates in [-1/2, 1/2) (NaN fails the comparison) and, with
@@ -44,7 +50,7 @@ template <int D>
 __device__ __forceinline__ bool node_key_fast(const double* xv, const KeyParams& kp, uint32_t& key) {
   bool ok = true;
   key = 0;
-  uint32_t cy = 0;
+  uint32_t cy = 0, cz = 0;
 #pragma unroll
   for (int t = 0; t < D; ++t) {
     const double v = xv[t];
@@ -55,15 +61,16 @@ __device__ __forceinline__ bool node_key_fast(const double* xv, const KeyParams&
     c = min(c, (int)kp.L - 1);
     key = key * (uint32_t)kp.nb[t] + ((uint32_t)c >> kp.log2W[t]);
     if (t == 1) cy = (uint32_t)c;
+    if (t == 2) cz = (uint32_t)c;
   }
-  if (D >= 2 && kp.colbits) key = (key << kp.colbits) | (cy & ((1u << kp.colbits) - 1u));
+  if (D >= 2 && kp.colbits) key = (key << kp.colbits) | minor_digit(cy, cz, kp.colbits);
   if (!ok) key = 0;
   return ok;
 }
 
 template <int D>
 __device__ __forceinline__ uint32_t node_key(const double* xv, const KeyParams& kp, int& code) {
-  uint32_t key = 0, cy = 0;
+  uint32_t key = 0, cy = 0, cz = 0;
   bool nonfinite = false, range = false, box = false;
 #pragma unroll
   for (int t = 0; t < D; ++t) {
@@ -76,8 +83,9 @@ __device__ __forceinline__ uint32_t node_key(const double* xv, const KeyParams& 
     c = min(c, (int)kp.L - 1);         // fl(L x) == L/2 for x < 1/2 (defensive)
     key = key * (uint32_t)kp.nb[t] + ((uint32_t)c >> kp.log2W[t]);
     if (t == 1) cy = (uint32_t)c;
+    if (t == 2) cz = (uint32_t)c;
   }
-  if (D >= 2 && kp.colbits) key = (key << kp.colbits) | (cy & ((1u << kp.colbits) - 1u));
+  if (D >= 2 && kp.colbits) key = (key << kp.colbits) | minor_digit(cy, cz, kp.colbits);
   code = nonfinite ? BAD_NOT_FINITE : range ? BAD_RANGE : box ? BAD_BOX : 0;
   return code ? 0u : key;
 }
@@ -102,7 +110,11 @@ __device__ __forceinline__ float4 node_rec3(const double* xv, const KeyParams& k
     u[t] = (float)w;
     c[t] = ci;
   }
-  return make_float4(u[0], u[1], u[2], __uint_as_float((uint32_t)(((c[1] & 15) << 3) | (c[2] & 7))));
+  // cell position in the bin: (column << 3 | z offset) for gather3y; (minor digit << 2 | z offset inside
+  // the half) for gather3q
+  const uint32_t md = kp.colbits == 5 ? ((minor_digit((uint32_t)c[1], (uint32_t)c[2], 5) << 2) | (uint32_t)(c[2] & 3))
+                                      : (uint32_t)(((c[1] & 15) << 3) | (c[2] & 7));
+  return make_float4(u[0], u[1], u[2], __uint_as_float(md));
 }
 
 template <int D>
@@ -562,7 +574,7 @@ __global__ void build_kernel(const double* __restrict__ x, const uint32_t* __res
 
 static int grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148LL * 32));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)sm_count() * 32));
 }
 
 // K2b for d = 1 one-pass plans (d1_binned): the keys are recomputed from x (exactly as K1 computed

@@ -88,18 +88,19 @@ def _sweep_inputs(kind, M, N, seed):
 
 
 KERNEL3 = {"y": ("gather3y_kernel", None), "c": ("gather3c_kernel", "BNFFT_GATHER3C"),
-           "s": ("gather3s_kernel", "BNFFT_GATHER3S")}
+           "s": ("gather3s_kernel", "BNFFT_GATHER3S"), "q": ("gather3q_kernel", "BNFFT_GATHER3Q")}
 
 
 def _use_kernel3(monkeypatch, which):
     monkeypatch.delenv("BNFFT_GATHER3C", raising=False)
     monkeypatch.delenv("BNFFT_GATHER3S", raising=False)
+    monkeypatch.delenv("BNFFT_GATHER3Q", raising=False)
     env = KERNEL3[which][1]
     if env:
         monkeypatch.setenv(env, "1")
 
 
-@pytest.mark.parametrize("which", ["y", "s"])
+@pytest.mark.parametrize("which", ["y", "s", "q"])
 @pytest.mark.parametrize("kind", ["uniform", "one_bin", "one_xline", "one_cell", "grid_nodes", "edges", "sparse"])
 def test_sweep3_parity(bn, torch, kind, which, monkeypatch):
     M, m = 32, 4
@@ -120,16 +121,17 @@ def test_sweep3_parity(bn, torch, kind, which, monkeypatch):
     plan.close()
 
 
+@pytest.mark.parametrize("which", ["y", "q"])
 @pytest.mark.parametrize("M", [8, 24, 32])
-def test_ysweep3_grid_sizes(bn, torch, M, monkeypatch):
+def test_ysweep3_grid_sizes(bn, torch, M, which, monkeypatch):
     """L = 16 (one item), L = 48 (partial y bins and a partial 8-x-line item), L = 64."""
     m, N = 4, 5000
     x = _sweep_inputs("uniform", M, N, 13)
     cfg = synth.CONFIGS[4].scaled(M=M, N=N)
     fh = synth.make_spectrum(cfg, variant=5, prec="c64")
-    _use_kernel3(monkeypatch, "y")
+    _use_kernel3(monkeypatch, which)
     f, plan = gpu_run(bn, torch, x, fh, M, m, "c64")
-    assert bn.GATHER_KERNELS[plan.info().gather_kernel].endswith("gather3y_kernel")
+    assert bn.GATHER_KERNELS[plan.info().gather_kernel].endswith(KERNEL3[which][0])
     assert rel_l2(f, oracle_f(x, fh, M, m)) <= TOL["c64"]
     plan.close()
 
