@@ -457,6 +457,7 @@ def run_gpu(args):
         obj = [bn.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         comm = bn.nccl_comm_init(obj[0], world, rank, local)
+        bn.nccl_selftest(comm, 1 << 20, stream.cuda_stream)   # fail early and loudly, not inside a timed step
         dist_kw = dict(rank=rank, nranks=world, nccl_comm=comm, dist="slab")
 
     sampler = ClockSampler(local)

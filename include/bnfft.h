@@ -287,11 +287,16 @@ BNFFT_API int bnfft_destroy(struct bnfft_plan_s* plan);
  * bnfft_nccl_comm_init: ncclCommInitRank on `device`; *comm_out is an ncclComm_t for bnfft_opts.
  * bnfft_nccl_comm_destroy: ncclCommDestroy.  NCCL is loaded at run time (libnccl.so.2, the copy
  * already in the process if any); without it these return BNFFT_E_NCCL.
+ * bnfft_nccl_selftest: collective check of the library's NCCL transport on `comm` (every rank of the
+ * communicator calls it): each rank sends `bytes` bytes to every rank including itself through the
+ * grouped ncclSend / ncclRecv exchange the slab path uses, and checks what it received and the host
+ * all-gather; stream-ordered on `stream` (a cudaStream_t, may be NULL), synchronous.
  * bnfft_group_create / destroy: an in-process group of nranks ranks; each rank's plan is created
  * and driven by its own host thread (collective calls block until every rank has arrived). */
 BNFFT_API int bnfft_nccl_unique_id(void* out128);
 BNFFT_API int bnfft_nccl_comm_init(const void* id128, int32_t nranks, int32_t rank, int32_t device, void** comm_out);
 BNFFT_API int bnfft_nccl_comm_destroy(void* comm);
+BNFFT_API int bnfft_nccl_selftest(void* comm, int64_t bytes, void* stream);
 BNFFT_API int bnfft_group_create(int32_t nranks, void** group_out);
 BNFFT_API int bnfft_group_destroy(void* group);
 

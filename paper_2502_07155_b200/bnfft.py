@@ -108,6 +108,7 @@ _sig = {
     "bnfft_nccl_unique_id": (c_int, [c_void_p]),
     "bnfft_nccl_comm_init": (c_int, [c_void_p, c_int32, c_int32, c_int32, POINTER(c_void_p)]),
     "bnfft_nccl_comm_destroy": (c_int, [c_void_p]),
+    "bnfft_nccl_selftest": (c_int, [c_void_p, c_int64, c_void_p]),
     "bnfft_group_create": (c_int, [c_int32, POINTER(c_void_p)]),
     "bnfft_group_destroy": (c_int, [c_void_p]),
     "bnfft_slab_cuts": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p]),
@@ -386,6 +387,11 @@ def nccl_comm_init(uid: bytes, nranks: int, rank: int, device: int) -> int:
     buf = ctypes.create_string_buffer(uid, 128)
     check(bnfft_nccl_comm_init(buf, nranks, rank, device, ctypes.byref(h)), "bnfft_nccl_comm_init")
     return h.value
+
+
+def nccl_selftest(comm: int, nbytes: int = 1 << 20, stream: int = 0) -> None:
+    """Collective check of the library's NCCL transport (bnfft_nccl_selftest); raises on failure."""
+    check(bnfft_nccl_selftest(comm, nbytes, stream), "bnfft_nccl_selftest")
 
 
 def nccl_comm_destroy(comm: int) -> None:

@@ -987,6 +987,67 @@ int bnfft_nccl_comm_destroy(void* comm) {
   return r == ncclSuccess ? BNFFT_OK : nccl_fail(r, "ncclCommDestroy");
 }
 
+// Collective self-test of the NCCL transport (header: bnfft_nccl_selftest): the library's own exchange and
+// all-gather code over `comm`, every rank sending `bytes` bytes to every rank (itself included).
+int bnfft_nccl_selftest(void* comm, int64_t bytes, void* stream) {
+  if (!comm || bytes < 1 || bytes > ((int64_t)1 << 30)) return BNFFT_E_INVALID_ARG;
+  NcclApi* a = nccl_api();
+  if (!a) {
+    set_error("libnccl.so.2 could not be loaded");
+    return BNFFT_E_NCCL;
+  }
+  NcclTransport t;
+  t.comm = (ncclComm_t)comm;
+  ncclResult_t r = a->CommCount(t.comm, &t.nranks);
+  if (r == ncclSuccess) r = a->CommUserRank(t.comm, &t.rank);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommCount");
+  cudaGetDevice(&t.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nb = (size_t)bytes, P = (size_t)t.nranks;
+  unsigned char *d_src = nullptr, *d_dst = nullptr;
+  cudaError_t e = cudaMalloc((void**)&d_src, nb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&d_dst, nb * P);
+  std::vector<unsigned char> h(nb), back(nb * P);
+  for (size_t i = 0; i < nb; ++i) h[i] = (unsigned char)(t.rank * 37 + i * 11 + (i >> 8));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_src, h.data(), nb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_dst, 0xee, nb * P, s);
+  int rc = e == cudaSuccess ? BNFFT_OK : cuda_fail(e, "selftest buffers");
+  if (rc == BNFFT_OK) {
+    std::vector<XOp> ops;
+    for (int q = 0; q < t.nranks; ++q) {
+      ops.push_back({true, q, d_src, nb});
+      ops.push_back({false, q, d_dst + (size_t)q * nb, nb});
+    }
+    rc = t.exchange(ops, s);
+  }
+  if (rc == BNFFT_OK) {
+    e = cudaMemcpyAsync(back.data(), d_dst, nb * P, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "selftest copy");
+  }
+  if (rc == BNFFT_OK) {
+    for (size_t q = 0; q < P && rc == BNFFT_OK; ++q)
+      for (size_t i = 0; i < nb; ++i)
+        if (back[q * nb + i] != (unsigned char)(q * 37 + i * 11 + (i >> 8))) {
+          set_error("NCCL self-test: wrong byte received from rank " + std::to_string(q));
+          rc = BNFFT_E_NCCL;
+          break;
+        }
+  }
+  if (rc == BNFFT_OK) {   // the host all-gather used for counts and cut points
+    int64_t mine[2] = {t.rank, bytes + t.rank}, all[2 * kMaxRanks];
+    rc = t.allgather_host(mine, sizeof(mine), all, s);
+    for (int q = 0; q < t.nranks && rc == BNFFT_OK; ++q)
+      if (all[2 * q] != q || all[2 * q + 1] != bytes + q) {
+        set_error("NCCL self-test: wrong all-gather entry");
+        rc = BNFFT_E_NCCL;
+      }
+  }
+  cudaFree(d_src);
+  cudaFree(d_dst);
+  return rc;
+}
+
 int bnfft_group_create(int32_t nranks, void** group_out) {
   if (!group_out || nranks < 1 || nranks > kMaxRanks) return BNFFT_E_INVALID_ARG;
   bnfft_group_s* g = new bnfft_group_s();

@@ -321,3 +321,19 @@ def test_slab_rejects_bad_node_on_all_ranks(bn, torch):
     grp.close()
     assert codes[1] == (bn.BNFFT_E_NODE_OUT_OF_RANGE, 200)
     assert codes[0][0] == bn.BNFFT_E_NODE_OUT_OF_RANGE and codes[0][1] == -1
+
+
+# ----------------------------------------------------------------------------- NCCL transport
+def test_nccl_transport_selftest(bn, torch):
+    """The library's NCCL transport (run-time libnccl, communicator init, grouped ncclSend/ncclRecv
+    exchange, host all-gather) on a one-rank communicator: every call the slab path makes over NCCL,
+    with this rank as its own peer (NCCL refuses two ranks on one GPU, so more ranks need more GPUs;
+    the slab logic itself runs over the in-process transport above)."""
+    torch.cuda.set_device(0)
+    torch.zeros(1, device="cuda:0")
+    comm = bn.nccl_comm_init(bn.nccl_unique_id(), 1, 0, 0)
+    try:
+        for nbytes in (1, 4096, (1 << 22) + 3):
+            bn.nccl_selftest(comm, nbytes, torch.cuda.current_stream().cuda_stream)
+    finally:
+        bn.nccl_comm_destroy(comm)
