@@ -180,7 +180,8 @@ enum {
   BNFFT_GK_PRE1 = 5,      /* d = 1 with BNFFT_PRECOMPUTE_PSI (gather1_kernel, stored taps)  */
   BNFFT_GK_SWEEP3 = 6,    /* d = 3, m = 4, complex64: z-sweep kernel (gather3s_kernel)       */
   BNFFT_GK_YSWEEP3 = 7,   /* d = 3, m = 4, complex64: y-sweep kernel (gather3y_kernel)       */
-  BNFFT_GK_YSWEEP3Q = 8   /* the same with half-height z sweeps, no z dispatch (gather3q_kernel) */
+  BNFFT_GK_YSWEEP3Q = 8,  /* the same with half-height z sweeps, no z dispatch (gather3q_kernel) */
+  BNFFT_GK_COOP2 = 9      /* d = 2, complex64, m <= 7: quarter-warp-cooperative kernel (gather2c) */
 };
 
 /* Per-stage device times (ms) accumulated since the last reset, and call counts.  Only

@@ -68,7 +68,7 @@ class bnfft_info(ctypes.Structure):
 GATHER_KERNELS = {0: "bnfft::gather1_kernel", 1: "bnfft::gather1b_kernel", 2: "bnfft::gather_kernel",
                   3: "bnfft::gatherN_kernel", 4: "bnfft::gather3c_kernel", 5: "bnfft::gather1_kernel",
                   6: "bnfft::gather3s_kernel", 7: "bnfft::gather3y_kernel",
-                  8: "bnfft::gather3q_kernel"}
+                  8: "bnfft::gather3q_kernel", 9: "bnfft::gather2c_kernel"}
 
 
 class bnfft_timing(ctypes.Structure):

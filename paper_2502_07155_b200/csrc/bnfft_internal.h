@@ -160,6 +160,7 @@ struct bnfft_plan_s {
   int gather_nslice = 1, gather_box_elems = 0, gather_bufstride = 0;
   int gather_nbuf = 2;
   int gather_threads = 256;      // threads per CTA of the d >= 2 gather launch
+  bool g2_coop = false;          // d = 2, complex64, batch 1, m <= 7: quarter-warp-cooperative kernel (gather2c)
   int g3_kind = 0;               // d = 3, m = 4, complex64, batch 1: 0 y-sweep (gather3y, default),
                                  // 1 half-warp (gather3c, BNFFT_GATHER3C), 2 z-sweep (gather3s, BNFFT_GATHER3S)
   int gather_tbox[3] = {1, 1, 1};

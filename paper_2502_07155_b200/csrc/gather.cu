@@ -19,6 +19,10 @@ size_t gather3y_smem();
 int gather3y_threads();
 void gather3y_box(int* ext);
 const void* gather3q_kernel_ptr(bool poly);
+const void* gather2c_kernel_ptr(int m, bool poly);
+size_t gather2c_stash_bytes(int threads);
+int gather2c_pad_bytes();
+int gather2c_max_m();
 size_t gather3q_smem();
 void gather3y_item_table(int64_t nX, int64_t nY, int64_t nZ, std::vector<uint32_t>& tab);
 
@@ -37,6 +41,10 @@ static const void* coop3_kernel(const bnfft_plan_s* p) {
   if (p->g3_kind == 2) return gather3s_kernel_ptr(p->tap_poly);
   return p->tap_poly ? gather3c_kernel_p() : gather3c_kernel_e();
 }
+
+// d = 2, complex64, batch 1, m <= 7: the quarter-warp-cooperative box kernel (gather2c.cu) unless
+// BNFFT_GATHER2N selects the thread-per-node kernel gatherN (chosen at plan creation: p->g2_coop)
+static bool use_coop2(const bnfft_plan_s* p) { return p->g2_coop; }
 
 static const void* select_kernel(int d, int m, bool c128, bool poly, bool batched = false, bool pre = false,
                                 bool binned = false) {
@@ -88,7 +96,7 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   const size_t budget = 48u << 10;              // bytes per staging buffer
   int bt = (int)std::max<size_t>(1, std::min<size_t>((size_t)p->opts.batch, budget / per));
   if (bt > 256) bt = 256;
-  const size_t buf_bytes = (per * bt + 127) & ~(size_t)127;
+  const size_t buf_bytes = (per * bt + (use_coop2(p) ? (size_t)gather2c_pad_bytes() : 0) + 127) & ~(size_t)127;
   // coop kernel: one box buffer, more CTAs per SM; gatherN: a ring of up to kMaxBoxBufs buffers
   // (mbarrier-released, see gatherN_kernel) within 100 KB (at least two)
   int nbuf = 1;
@@ -96,6 +104,7 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
     nbuf = 3 * buf_bytes <= ((size_t)100 << 10) ? 3 : 2;
     if (const char* s = getenv("BNFFT_BOX_BUFS")) nbuf = std::max(2, std::min(kMaxBoxBufs, atoi(s)));   // tuning knob
   }
+  if (use_coop2(p) && !getenv("BNFFT_BOX_BUFS")) nbuf = 2;   // measured best with 64-thread CTAs (cfg3)
   p->gather_nbuf = nbuf;
   p->gather_bt = bt;
   p->gather_nslice = (p->opts.batch + bt - 1) / bt;
@@ -104,9 +113,14 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   for (int t = 0; t < 3; ++t) p->gather_tbox[t] = t < d ? ext[t] : 1;
   p->gather_smem = use_sweep3(p) ? gather3s_smem() : use_ysweep3(p) ? (p->g3_kind == 3 ? gather3q_smem() : gather3y_smem()) : nbuf * buf_bytes;
   p->gather_threads = use_sweep3(p) ? gather3s_threads() : use_ysweep3(p) ? gather3y_threads() : kGatherThreads;
+  if (use_coop2(p)) {   // small CTAs: a uniform cfg3 item (~64 nodes) is one batch per warp (knob: 64..256)
+    p->gather_threads = 64;
+    if (const char* s = getenv("BNFFT_GATHER2C_THREADS")) p->gather_threads = std::max(32, std::min(256, atoi(s) / 32 * 32));
+    p->gather_smem += gather2c_stash_bytes(p->gather_threads);
+  }
   // tuning knob: 128-thread box CTAs (measured equal to 256 on cfg3: the kernel is latency-bound on
   // the node loads and box hand-offs, not on idle threads of sparse bins)
-  if (!use_coop3(p))
+  if (!use_coop3(p) && !use_coop2(p))
     if (const char* s = getenv("BNFFT_GATHERN_THREADS")) p->gather_threads = atoi(s) == 128 ? 128 : 256;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
   if (e != cudaSuccess) return e;
@@ -180,6 +194,7 @@ cudaError_t gather_prepare(bnfft_plan_s* p) {
   const void* fn = select_kernel(p->opts.d, p->opts.m, p->c128, p->tap_poly, p->opts.batch > 1,
                                  (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0, p->d1_binned);
   if (use_coop3(p)) fn = coop3_kernel(p);
+  if (use_coop2(p)) fn = gather2c_kernel_ptr(p->opts.m, p->tap_poly);
   if (!fn) return cudaErrorInvalidValue;
   if (p->d1_binned) {
     // one window per bin (bin + halo, 16-byte aligned), double-buffered; persistent grid by occupancy
@@ -341,6 +356,7 @@ cudaError_t launch_gather(bnfft_plan_s* p, void* out) {
                                  (p->opts.flags & BNFFT_PRECOMPUTE_PSI) != 0, p->d1_binned);
   // d = 3, m = 4, complex64: the kernel chosen at plan creation (its launch shape is in the plan)
   if (use_coop3(p)) fn = coop3_kernel(p);
+  if (use_coop2(p)) fn = gather2c_kernel_ptr(p->opts.m, p->tap_poly);
   if (!fn) return cudaErrorInvalidValue;
   return p->c128 ? launch_gather_t<double>(p, out, fn) : launch_gather_t<float>(p, out, fn);
 }

@@ -392,6 +392,7 @@ int bnfft_plan_create(const bnfft_opts* o, bnfft_plan_s** out) {
   p->g3_kind = getenv("BNFFT_GATHER3S") ? 2 : getenv("BNFFT_GATHER3C") ? 1 : getenv("BNFFT_GATHER3Q") ? 3 : 0;
   if ((p->g3_kind == 0 || p->g3_kind == 3) && L > 8192) p->g3_kind = 1;   // y-sweep item table: 10-bit item coordinates
   p->rec3 = coop3 && (p->g3_kind == 0 || p->g3_kind == 3);
+  p->g2_coop = o->d == 2 && o->prec == BNFFT_C64 && o->batch == 1 && o->m <= 7 && !getenv("BNFFT_GATHER2N");
   for (int t = 0; t < 3; ++t) {
     int lt = lg;
     if (coop3) lt = p->rec3 ? (t == 0 ? 0 : t == 1 ? 4 : 3) : (t == 2 ? 4 : 3);
@@ -965,7 +966,7 @@ int bnfft_get_info(const bnfft_plan_s* p, bnfft_info* o) {
                        : p->d1_binned ? BNFFT_GK_BIN1 : BNFFT_GK_WINDOW1;
   } else {
     const bool coop3 = p->opts.d == 3 && p->opts.m == 4 && !p->c128 && p->opts.batch == 1;
-    o->gather_kernel = !coop3 ? BNFFT_GK_BOX
+    o->gather_kernel = p->g2_coop ? BNFFT_GK_COOP2 : !coop3 ? BNFFT_GK_BOX
                        : p->g3_kind == 0 ? BNFFT_GK_YSWEEP3 : p->g3_kind == 3 ? BNFFT_GK_YSWEEP3Q
                        : p->g3_kind == 1 ? BNFFT_GK_COOP3 : BNFFT_GK_SWEEP3;
   }

@@ -337,3 +337,48 @@ def test_nccl_transport_selftest(bn, torch):
             bn.nccl_selftest(comm, nbytes, torch.cuda.current_stream().cuda_stream)
     finally:
         bn.nccl_comm_destroy(comm)
+
+
+# ----------------------------------------------------------------------------- d = 2 cooperative gather
+@pytest.mark.parametrize("m", [1, 2, 4, 6, 7, 8])
+@pytest.mark.parametrize("kind", ["mixed", "grid_nodes", "edges", "one_cell"])
+def test_gather2c_parity(bn, torch, m, kind, monkeypatch):
+    """d = 2 complex64: the quarter-warp kernel gather2c (m <= 7; gatherN beyond) against the oracle and,
+    bitwise for Kronecker nodes, against theta; BNFFT_GATHER2N selects gatherN."""
+    M, N = 64, 20_011
+    L = 2 * M
+    rng = np.random.default_rng(100 + m)
+    if kind == "mixed":          # cfg3's recipe: half uniform, half clustered around the origin
+        x = rng.random((N, 2)) - 0.5
+        x[N // 2:] = np.clip(0.05 * rng.standard_normal((N - N // 2, 2)), -0.5, 0.49)
+    elif kind == "grid_nodes":
+        x = rng.integers(-L // 2, L // 2, size=(N, 2)).astype(np.float64) / L
+    elif kind == "edges":        # windows reaching past the grid ends (zero extension, reading A5)
+        x = rng.random((N, 2)) - 0.5
+        x[: N // 2, 0] = -0.5 + rng.random(N // 2) * 3 / L
+        x[N // 2:, 1] = 0.5 - rng.random(N - N // 2) * 3 / L
+    else:                        # one cell: every batch reads the same window
+        x = (rng.random((3000, 2)) + np.array([-7, 21])) / L
+    x = np.clip(x, -0.5, np.nextafter(0.5, 0))
+    cfg = synth.CONFIGS[3].scaled(M=M, N=len(x), m=m)
+    fh = synth.make_spectrum(cfg, variant=4, prec="c64")
+    dev = torch.device("cuda:0")
+    xt, ft = torch.from_numpy(x).to(dev), torch.from_numpy(fh).to(dev)
+    plan = bn.Plan(2, M, 2.0, m, "sinh", "c64")
+    want = "gather2c_kernel" if m <= 7 else "gatherN_kernel"
+    assert bn.GATHER_KERNELS[plan.info().gather_kernel].endswith(want)
+    plan.set_nodes(xt)
+    f = plan.execute(ft).cpu().numpy()
+    ref = O.algorithm2(x, fh.astype(np.complex128), M, 2.0, m, "sinh")["f"]
+    assert rel_l2(f, ref) <= TOL["c64"]
+    if kind == "grid_nodes":     # interpolation property (P:328-333)
+        g = plan.grid().cpu().numpy()[0]
+        c = np.floor(L * x).astype(np.int64) + L // 2
+        assert np.array_equal(f[0], g[c[:, 0], c[:, 1]])
+    plan.close()
+    monkeypatch.setenv("BNFFT_GATHER2N", "1")
+    plan = bn.Plan(2, M, 2.0, m, "sinh", "c64")
+    assert bn.GATHER_KERNELS[plan.info().gather_kernel].endswith("gatherN_kernel")
+    plan.set_nodes(xt)
+    assert rel_l2(plan.execute(ft).cpu().numpy(), ref) <= TOL["c64"]
+    plan.close()
