@@ -15,4 +15,4 @@ NO="--no-variants --no-cpu --no-e2e --no-peaks"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gather3y -s 1 -c 1 -o gpurun_out/${TAG}_gather_cfg4 -f python bench.py --steps 1 --warmup 1 $NO > gpurun_out/${TAG}_ncu_g4.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:radix_scatter -s 2 -c 1 -o gpurun_out/${TAG}_sort_cfg4 -f python bench.py --steps 1 --warmup 1 $NO > gpurun_out/${TAG}_ncu_s4.log 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:gather1b -s 2 -c 1 -o gpurun_out/${TAG}_gather_cfg2 -f python bench.py --cfg 2 --steps 1 --warmup 3 $NO > gpurun_out/${TAG}_ncu_g2.log 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:gatherN -s 1 -c 1 -o gpurun_out/${TAG}_gather_cfg3 -f python bench.py --cfg 3 --steps 1 --warmup 2 $NO > gpurun_out/${TAG}_ncu_g3.log 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:gather2c -s 1 -c 1 -o gpurun_out/${TAG}_gather_cfg3 -f python bench.py --cfg 3 --steps 1 --warmup 2 $NO > gpurun_out/${TAG}_ncu_g3.log 2>&1
