@@ -502,6 +502,11 @@ def run_gpu(args):
         }
         if peaks:
             line["peaks"] = peaks
+        if world == 1 and THREE_CALLS:   # the same step through the one-call API, for comparison
+            ms1 = time_steps(torch, plan, res["x_dev"], res["fh_dev"], res["out"], args.steps, args.warmup, stream,
+                             three_calls=False) / args.steps
+            line["one_call"] = {"api": "bnfft_transform (grid stage on the side stream, concurrent with the sort)",
+                                "ms_per_step": ms1, "nodes_per_s": cfg.N * cfg.batch / (ms1 * 1e-3)}
 
     # ---- e2e through the pipelined host-buffer C-ABI call (pinned host memory): every step copies its
     # nodes and spectrum host->device and its result device->host; bnfft_transform_host_many overlaps
@@ -549,7 +554,13 @@ def run_gpu(args):
             vc, _, _ = workload(cid, vp, vw)
             ksteps, kwarm = (3, 2) if cid == 5 else (10, 3)
             r = run_config(torch, bn, vc, vp, vw, ksteps, kwarm, dev, local, stream, peaks)
-            var[f"cfg{cid}-{vw}-{vp}"] = summary(vc, vp, vw, r, ksteps, peaks)
+            sv = summary(vc, vp, vw, r, ksteps, peaks)
+            if cid != 5:   # the same work through the one-call API (grid stage concurrent with the sort)
+                ms1 = time_steps(torch, r["plan"], r["x_dev"], r["fh_dev"], r["out"], ksteps, kwarm, stream,
+                                 three_calls=False) / ksteps
+                sv["one_call"] = {"api": "bnfft_transform", "ms_per_step": ms1,
+                                  "nodes_per_s": vc.N * vc.batch / (ms1 * 1e-3)}
+            var[f"cfg{cid}-{vw}-{vp}"] = sv
             r["plan"].close()
             del r
             torch.cuda.empty_cache()
