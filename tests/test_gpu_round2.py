@@ -3,7 +3,11 @@
 * the d = 3, m = 4, complex64 gathers (y-sweep gather3y, the default; z-sweep gather3s): clustered
   node sets that overflow a bin's stash or an x-line's chunk, many nodes in one cell, grid nodes
   (Kronecker case), the global grid ends, sparse node sets, several grid sizes, and the half-warp
-  kernel gather3c (BNFFT_GATHER3C) as a further witness;
+  kernel gather3c (BNFFT_GATHER3C) and the half-height y-sweep gather3q (BNFFT_GATHER3Q) as further
+  witnesses;
+* the d = 2 complex64 quarter-warp kernel gather2c (m <= 7) and gatherN (BNFFT_GATHER2N, m = 8): cfg3's
+  mixed node recipe, grid nodes, the grid ends, one cell;
+* the NCCL transport's self-test on a one-rank communicator;
 * BNFFT_SORTED_OUTPUT: f_sorted[i] == f_user[perm[i]] bitwise;
 * repeated executes on d = 2 and d = 3 plans are bitwise equal (the FFT input's zero padding is
   written once at plan creation; ADVICE round 1);
