@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(g3y::NT, 1) gather3y_kernel(const __grid_const
 namespace g3q {
 
 constexpr int NW = g3y::NW, NT = NW * 32, NBUF = g3y::NBUF, T = 8;
-constexpr int BX = g3y::BX, BY = g3y::BY, BZ = g3y::BZ, BOX = g3y::BOX, BOXB = g3y::BOXB;
+constexpr int BY = g3y::BY, BZ = g3y::BZ, BOXB = g3y::BOXB;   // gather3y's box
 constexpr int RZ = 12;                     // z values per register row
 constexpr int REC = 28;                    // words per record: wz12[12] | wy pairs[8] | wx[8]  (112 B: the
                                            // 16-B slots of 8 consecutive lanes' records are distinct)
