@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather2c_kernel(const __grid_c
       first = false;
       __syncwarp();
       // ---- phase 2: quarter-warp qw contracts nodes qw, qw + 4, ...
+#pragma unroll 4
       for (int j0 = 0; j0 < nbn; j0 += 4) {   // (warp-uniform trip count: the shuffles below are full-warp)
         const bool live = j0 + qw < nbn;
         const int j = live ? j0 + qw : nbn - 1;
