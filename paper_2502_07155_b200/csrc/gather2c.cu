@@ -58,8 +58,9 @@ __global__ void __launch_bounds__(kGatherThreads) gather2c_kernel(const __grid_c
 
   // Items: the non-empty keys blockIdx.x + j G.  Thread 0 stages their boxes NB - 1 items ahead (ring and
   // mbarrier hand-off as gatherN_kernel); every thread also walks the sequence itself, one item ahead,
-  // so that the node data of the next item's first batch (permutation entry, coordinates) is loaded
-  // during the current item: no global-memory latency between an item's box and its contraction.
+  // and each warp loads the node data (permutation entry, coordinates) of its next batch -- in the
+  // same item, else the next item's first -- during the current batch: no global-memory latency
+  // between an item's box and its contraction, or between the batches of a large item.
   // (Measured slower on cfg3 and removed: claiming keys from a global counter, and splitting the
   // clustered centre's 4000-node bins into chunks that idle CTAs pick up -- the claim latency sits in
   // thread 0's staging path.)
@@ -85,6 +86,13 @@ __global__ void __launch_bounds__(kGatherThreads) gather2c_kernel(const __grid_c
   struct NodeData {
     uint32_t dst;
     double2 x;
+  };
+  auto fetch_at = [&](int64_t i0, int64_t ie, NodeData& nd) {   // node i0 + lane of a batch
+    const int64_t i = i0 + lane;
+    if (i < ie) {
+      nd.dst = __ldg(&p.perm[i]);
+      nd.x = __ldg(reinterpret_cast<const double2*>(p.xs) + (p.xs_user ? (int64_t)nd.dst : i));
+    }
   };
   auto fetch = [&](const Item& t, NodeData& nd) {   // node t.ib + 32 wid + lane (the warp's first batch)
     const uint32_t i = t.ib + (uint32_t)(32 * wid + lane);
@@ -118,7 +126,6 @@ __global__ void __launch_bounds__(kGatherThreads) gather2c_kernel(const __grid_c
       if (it >= 1) mbar_wait(&empty[bn], (uint32_t)((it - 1) / NB) & 1u);
       stage(bn);
     }
-    fetch(nxt, nd_nxt);                                  // in flight during this item
     const Item nn = nxt.u >= 0 ? item_from(nxt.u + G) : nxt;   // (its offsets are used next iteration)
     mbar_wait(&full[b], (uint32_t)(it / NB) & 1u);
     const int64_t u = cur.u;
@@ -128,21 +135,17 @@ __global__ void __launch_bounds__(kGatherThreads) gather2c_kernel(const __grid_c
     const int bo1 = (int)((rem % (uint32_t)p.nb[1]) << p.log2W[1]);
     const int shift1 = (bo1 - (m - 1)) & 1;   // even-aligned box start (issue_box)
     const int64_t i_beg = cur.ib, i_end = cur.ie;
-    bool first = true;
+    if (i_beg + 32 * wid >= i_end) fetch(nxt, nd_cur);   // no batch for this warp in this item
     for (int64_t i0 = i_beg + 32 * wid; i0 < i_end; i0 += 32 * nwarps) {
       const int nbn = (int)min((int64_t)32, i_end - i0);
+      // the warp's next batch (in this item, else the first one of the next item): in flight meanwhile
+      if (i0 + 32 * nwarps < i_end) fetch_at(i0 + 32 * nwarps, i_end, nd_nxt);
+      else fetch(nxt, nd_nxt);
       // ---- phase 1: lane = node i0 + lane
       if (lane < nbn) {
         const int64_t i = i0 + lane;
-        uint32_t dst;
-        double2 xv;
-        if (first) {
-          dst = nd_cur.dst;
-          xv = nd_cur.x;
-        } else {
-          dst = __ldg(&p.perm[i]);
-          xv = __ldg(reinterpret_cast<const double2*>(p.xs) + (p.xs_user ? (int64_t)dst : i));
-        }
+        const uint32_t dst = nd_cur.dst;
+        const double2 xv = nd_cur.x;
         int off[2];
         float w[2][T];
 #pragma unroll
@@ -175,7 +178,6 @@ __global__ void __launch_bounds__(kGatherThreads) gather2c_kernel(const __grid_c
           reinterpret_cast<float4*>(r)[5 + q] = make_float4(c16[4 * q], c16[4 * q + 1], c16[4 * q + 2], c16[4 * q + 3]);
         }
       }
-      first = false;
       __syncwarp();
       // ---- phase 2: quarter-warp qw contracts nodes qw, qw + 4, ...
 #pragma unroll 4
@@ -215,10 +217,10 @@ __global__ void __launch_bounds__(kGatherThreads) gather2c_kernel(const __grid_c
         if (l == 0 && live) out[hdr.y] = f;
       }
       __syncwarp();   // stash free for the next batch
+      nd_cur = nd_nxt;
     }
     mbar_arrive(&empty[b]);
     cur = nxt;
-    nd_cur = nd_nxt;
     nxt = nn;
   }
 }
