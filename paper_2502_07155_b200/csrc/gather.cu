@@ -121,7 +121,7 @@ static cudaError_t gatherN_prepare(bnfft_plan_s* p, const void* fn) {
   // tuning knob: 128-thread box CTAs (measured equal to 256 on cfg3: the kernel is latency-bound on
   // the node loads and box hand-offs, not on idle threads of sparse bins)
   if (!use_coop3(p) && !use_coop2(p))
-    if (const char* s = getenv("BNFFT_GATHERN_THREADS")) p->gather_threads = atoi(s) == 128 ? 128 : 256;
+    if (const char* s = getenv("BNFFT_GATHERN_THREADS")) p->gather_threads = std::max(32, std::min(256, atoi(s) / 32 * 32));
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->gather_smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0, nsm = 0, dev = 0;
