@@ -33,7 +33,7 @@ int gather2c_pad_bytes() { return g2c::PADB; }
 int gather2c_max_m() { return 7; }
 
 template <int T, bool POLY>
-__global__ void __launch_bounds__(kGatherThreads) gather2c_kernel(const __grid_constant__ GatherParams<float> p,
+__global__ void __launch_bounds__(kGatherThreads, 3) gather2c_kernel(const __grid_constant__ GatherParams<float> p,
                                                                   const CUtensorMap* __restrict__ tmap) {
   using namespace g2c;
   using C = float2;
