@@ -134,8 +134,10 @@ typedef struct {
 /* Plan description.  Node binning geometry (for the stable bin sort, row a1): the cell of
  * a node is c_t = floor(L x_t) + L/2 in [0, L) (clamped to L-1), its bin b_t = c_t >> bin_log2[t],
  * its bin index is row-major (dim 0 slowest) over bins_per_dim, and its sort key is
- * ((j >> user_block_log2) * nbins + bin) * 2^key_col_bits + (c_1 mod 2^key_col_bits) for user index
- * j (key_col_bits = 4 for the d = 3 y-sweep gather: an x-line bin's nodes in y-column order, else 0).
+ * ((j >> user_block_log2) * nbins + bin) * 2^key_col_bits + minor for user index j, where minor =
+ * c_1 mod 16 for key_col_bits = 4 (the d = 3 y-sweep gather: an x-line bin's nodes in y-column order),
+ * minor = ((c_2 >> 2) & 1) * 16 + c_1 mod 16 for key_col_bits = 5 (gather3q: two column sweeps, one per
+ * half of the bin's z extent), and no minor digit for key_col_bits = 0.
  * Nodes are sorted stably by that key (ties by user index); the key offsets (bnfft_get_bin_offsets)
  * are per (user block, bin): nkeys = ceil(n / 2^user_block_log2) * nbins for the current node set.
  * tap_poly: the gather evaluates psi by per-tap polynomials (fit error tap_fit_err, checked at

@@ -386,3 +386,27 @@ def test_gather2c_parity(bn, torch, m, kind, monkeypatch):
     plan.set_nodes(xt)
     assert rel_l2(plan.execute(ft).cpu().numpy(), ref) <= TOL["c64"]
     plan.close()
+
+
+def test_gather3q_sort_bit_exact(bn, torch, monkeypatch):
+    """The gather3q plan's sort key (bin, (z half, y column)) as documented in include/bnfft.h: the
+    permutation and the key offsets equal the oracle's stable sort bit for bit."""
+    M, N = 64, 50_000
+    cfg = synth.CONFIGS[4].scaled(M=M, N=N)
+    x = synth.make_nodes(cfg, variant=2)
+    x[:300] = 0.0   # a run of identical keys (ties by user index)
+    _use_kernel3(monkeypatch, "q")
+    plan = bn.Plan(3, M, 2.0, 4, "sinh", "c64")
+    plan.set_nodes(torch.from_numpy(x).cuda())
+    info = plan.info()
+    assert int(info.key_col_bits) == 5
+    cells = np.minimum(O.cell_index(x, info.L), info.L - 1)
+    key = np.zeros(N, dtype=np.int64)
+    for t in range(3):
+        key = key * info.bins_per_dim[t] + (cells[:, t] >> info.bin_log2[t])
+    minor = (((cells[:, 2] >> 2) & 1) << 4) | (cells[:, 1] & 15)
+    perm_ref, _ = O.stable_bin_sort(key * 32 + minor, int(info.nkeys) << 5)
+    _, off_ref = O.stable_bin_sort(key, int(info.nkeys))
+    assert np.array_equal(plan.perm().cpu().numpy().astype(np.int64), perm_ref)
+    assert np.array_equal(plan.bin_offsets().cpu().numpy().astype(np.int64), off_ref)
+    plan.close()
