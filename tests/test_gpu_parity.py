@@ -257,6 +257,26 @@ def test_transform_one_call(bn, torch, d, M, m, prec, N):
     ref_plan.close()
 
 
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_transform_empty_and_single_node(bn, torch, d):
+    """bnfft_transform with n = 0 (nothing written) and n = 1, then a regular node set on the same plan."""
+    M, m = (256, 4) if d == 1 else (32, 4)
+    cfg = synth.CONFIGS[{1: 2, 2: 3, 3: 4}[d]].scaled(M=M, N=5000, m=m)
+    dev = torch.device("cuda:0")
+    fh = synth.make_spectrum(cfg, variant=2, prec="c64")
+    ft = torch.from_numpy(fh).to(dev)
+    x = synth.make_nodes(cfg, variant=2)
+    plan = bn.Plan(d, M, 2.0, m, "sinh", "c64")
+    f0 = plan.transform(torch.empty((0, d), dtype=torch.float64, device=dev), ft)
+    assert f0.shape == (1, 0)
+    f1 = plan.transform(torch.from_numpy(x[:1].copy()).to(dev), ft).cpu().numpy()
+    fa = plan.transform(torch.from_numpy(x).to(dev), ft).cpu().numpy()
+    ref = oracle_f(x, fh, M, 2.0, m, "sinh")["f"]
+    assert rel_l2(fa, ref) <= TOL["c64"]
+    assert abs(f1[0, 0] - ref[0, 0]) <= 1e-5 * np.abs(ref).max()
+    plan.close()
+
+
 @pytest.mark.parametrize("d,M,m,prec", [(1, 1 << 10, 8, "c64"), (3, 16, 4, "c64"), (2, 32, 5, "c128")])
 def test_transform_host_many_pipelined(bn, torch, d, M, m, prec):
     """bnfft_transform_host_many: five steps with different node sets and spectra, each equal bitwise
