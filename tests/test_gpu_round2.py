@@ -410,3 +410,21 @@ def test_gather3q_sort_bit_exact(bn, torch, monkeypatch):
     assert np.array_equal(plan.perm().cpu().numpy().astype(np.int64), perm_ref)
     assert np.array_equal(plan.bin_offsets().cpu().numpy().astype(np.int64), off_ref)
     plan.close()
+
+
+@pytest.mark.parametrize("M,m", [(4, 2), (14, 4), (8, 7), (24, 6)])
+def test_gather2c_small_grids(bn, torch, M, m):
+    """d = 2 grids smaller than or not a multiple of the 16-cell bins (L = 8, 28, 16, 48): partial bins,
+    windows mostly outside the grid (zero extension, reading A5)."""
+    N = 4001
+    rng = np.random.default_rng(7 * M + m)
+    x = np.clip(rng.random((N, 2)) - 0.5, -0.5, np.nextafter(0.5, 0))
+    cfg = synth.CONFIGS[3].scaled(M=M, N=N, m=m)
+    fh = synth.make_spectrum(cfg, variant=6, prec="c64")
+    dev = torch.device("cuda:0")
+    plan = bn.Plan(2, M, 2.0, m, "sinh", "c64")
+    assert bn.GATHER_KERNELS[plan.info().gather_kernel].endswith("gather2c_kernel")
+    f = plan.transform(torch.from_numpy(x).to(dev), torch.from_numpy(fh).to(dev)).cpu().numpy()
+    ref = O.algorithm2(x, fh.astype(np.complex128), M, 2.0, m, "sinh")["f"]
+    assert rel_l2(f, ref) <= TOL["c64"]
+    plan.close()
